@@ -1,0 +1,441 @@
+"""Python mirror of the reference's C++ entry points (proj/include/nufft/*.hpp),
+over the C-ABI of libnufft_b200.so.  Names, argument meaning and error
+behaviour follow the reference: std::invalid_argument -> InvalidArgument,
+std::domain_error -> DomainError (both ValueError subclasses).
+
+Host-array calls (numpy) copy to and from the GPU; the ``*_device`` methods
+take device pointers (e.g. ``torch.Tensor.data_ptr()``) and a CUDA stream
+handle, which is the path the throughput metric is measured on.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import PlanInfo, lib
+
+__all__ = [
+    "InvalidArgument", "DomainError", "NufftError",
+    "lambert_w", "bessel_j_int", "bessel_j_signed", "select_rank", "cheb_coefficients",
+    "cheb_eval_matrix", "build_factors", "fft_forward", "fft_inverse", "fft_2d_forward",
+    "fft_cols_forward", "fft_rows_forward", "fft_exec_count", "fft_reset_exec_counts",
+    "normalize_samples", "grid_assign", "Plan2", "Plan1", "Plan3", "Plan2D",
+    "plan_nufft2", "exec_nufft2", "exec_nufft2_adjoint", "plan_nufft1", "exec_nufft1",
+    "plan_nufft3", "exec_nufft3", "plan_nufft2d2", "exec_nufft2d2", "exec_nufft2d2_impl",
+    "device_count",
+]
+
+
+class NufftError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DomainError(ValueError):
+    """std::domain_error in the reference."""
+
+
+class CudaError(NufftError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().nufft_last_error().decode()
+    if rc == 1:
+        raise InvalidArgument(msg)
+    if rc == 2:
+        raise DomainError(msg)
+    if rc == 3:
+        raise CudaError(msg)
+    raise NufftError(f"status {rc}: {msg}")
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data if a.size else None
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().nufft_device_count(C.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------------------ special
+def lambert_w(x: float) -> float:
+    out = C.c_double()
+    _check(lib().nufft_lambert_w(x, C.byref(out)))
+    return out.value
+
+
+def bessel_j_int(order: int, z: float) -> float:
+    out = C.c_double()
+    _check(lib().nufft_bessel_j_int(order, z, C.byref(out)))
+    return out.value
+
+
+def bessel_j_signed(order: int, z: float) -> float:
+    out = C.c_double()
+    _check(lib().nufft_bessel_j_signed(order, z, C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ lowrank
+def select_rank(gamma: float, epsilon: float) -> int:
+    k = C.c_size_t()
+    _check(lib().nufft_select_rank(gamma, epsilon, C.byref(k)))
+    return k.value
+
+
+def cheb_coefficients(gamma: float, K: int) -> np.ndarray:
+    """K x K complex, a[p, r] (lowrank.hpp:36-65)."""
+    a = np.zeros((K, K), np.complex128)
+    _check(lib().nufft_cheb_coefficients(gamma, K, a.ctypes.data))
+    return a
+
+
+def cheb_eval_matrix(points, K: int) -> np.ndarray:
+    p = _f64(points)
+    out = np.zeros((len(p), K))
+    _check(lib().nufft_cheb_eval_matrix(_ptr(p), len(p), K, _ptr(out)))
+    return out
+
+
+def build_factors(delta, gamma: float, omega_scaled, epsilon: float):
+    """(rank, u[K, n], v[K, m]) — lowrank.hpp:161-210."""
+    d, w = _f64(delta), _f64(omega_scaled)
+    k = C.c_size_t()
+    _check(lib().nufft_build_factors(_ptr(d), len(d), gamma, _ptr(w), len(w), epsilon,
+                                     C.byref(k), None, None))
+    u = np.zeros((k.value, len(d)), np.complex128)
+    v = np.zeros((k.value, len(w)), np.complex128)
+    _check(lib().nufft_build_factors(_ptr(d), len(d), gamma, _ptr(w), len(w), epsilon,
+                                     C.byref(k), _ptr(u), _ptr(v)))
+    return k.value, u, v
+
+
+# ------------------------------------------------------------------ fft
+def fft_forward(v) -> np.ndarray:
+    v = _c128(v)
+    out = np.empty_like(v)
+    _check(lib().nufft_fft_forward_host(_ptr(v), _ptr(out), len(v)))
+    return out
+
+
+def fft_inverse(v) -> np.ndarray:
+    v = _c128(v)
+    out = np.empty_like(v)
+    _check(lib().nufft_fft_inverse_host(_ptr(v), _ptr(out), len(v)))
+    return out
+
+
+def fft_2d_forward(m) -> np.ndarray:
+    m = _c128(m)
+    if m.ndim != 2:
+        raise InvalidArgument("fft_2d_forward: expected a matrix")
+    out = np.empty_like(m)
+    _check(lib().nufft_fft_2d_forward_host(_ptr(m), _ptr(out), m.shape[0], m.shape[1]))
+    return out
+
+
+def fft_cols_forward(m) -> np.ndarray:
+    out = _c128(m).copy()
+    _check(lib().nufft_fft_cols_forward_host(_ptr(out), out.shape[0], out.shape[1]))
+    return out
+
+
+def fft_rows_forward(m) -> np.ndarray:
+    out = _c128(m).copy()
+    _check(lib().nufft_fft_rows_forward_host(_ptr(out), out.shape[0], out.shape[1]))
+    return out
+
+
+def fft_exec_count(n: int) -> int:
+    return int(lib().nufft_fft_exec_count(n))
+
+
+def fft_reset_exec_counts() -> None:
+    lib().nufft_fft_reset_exec_counts()
+
+
+# ------------------------------------------------------------------ samples
+def normalize_samples(raw) -> np.ndarray:
+    r = _f64(raw)
+    out = np.zeros_like(r)
+    _check(lib().nufft_normalize_samples(_ptr(r), len(r), _ptr(out)))
+    return out
+
+
+def grid_assign(x, grid: int):
+    """(s, t, gamma) — transforms.hpp:77-92."""
+    x = _f64(x)
+    s = np.zeros(len(x), np.int64)
+    t = np.zeros(len(x), np.uint64)
+    g = C.c_double()
+    _check(lib().nufft_grid_assign(_ptr(x), len(x), grid, _ptr(s), _ptr(t), C.byref(g)))
+    return s, t, g.value
+
+
+# ------------------------------------------------------------------ plans
+class _PlanBase:
+    _kind = ""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        self._info = PlanInfo()
+        _check(getattr(lib(), f"nufft_{self._kind}_info")(self._h, C.byref(self._info)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                getattr(lib(), f"nufft_{self._kind}_destroy")(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def info(self) -> PlanInfo:
+        return self._info
+
+    def size(self) -> int:
+        return self._info.n
+
+    @property
+    def device(self) -> int:
+        return self._info.device
+
+    @property
+    def fused(self) -> bool:
+        return self._info.path == 1
+
+
+class Plan2(_PlanBase):
+    """Type-II plan (transforms.hpp:105-114)."""
+    _kind = "plan2"
+
+    def rank(self) -> int:
+        return self._info.rank
+
+    def gamma(self) -> float:
+        return self._info.gamma
+
+    def samples(self):
+        n = self.size()
+        x, s, t = np.zeros(n), np.zeros(n, np.int64), np.zeros(n, np.uint64)
+        _check(lib().nufft_plan2_samples(self._h, _ptr(x), _ptr(s), _ptr(t)))
+        return x, s, t
+
+    def factors(self):
+        K, n = self.rank(), self.size()
+        u, v = np.zeros((K, n), np.complex128), np.zeros((K, n), np.complex128)
+        _check(lib().nufft_plan2_factors(self._h, _ptr(u), _ptr(v)))
+        return u, v
+
+    def execute(self, c, threads: int = 1) -> np.ndarray:
+        c = _c128(c)
+        batch = 1 if c.ndim == 1 else c.shape[0]
+        length = c.shape[-1]
+        f = np.empty_like(c)
+        _check(lib().nufft_plan2_exec_host(self._h, _ptr(c), length, _ptr(f), batch))
+        return f
+
+    def execute_device(self, c_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
+        _check(lib().nufft_plan2_exec(self._h, c_ptr, f_ptr, batch, stream or None))
+
+    def execute_terms_device(self, c_ptr: int, f_ptr: int, r_begin: int, r_end: int,
+                             batch: int = 1, stream: int = 0) -> None:
+        _check(lib().nufft_plan2_exec_terms(self._h, c_ptr, f_ptr, batch, r_begin, r_end,
+                                            stream or None))
+
+    def execute_timed_device(self, c_ptr: int, f_ptr: int, stream: int, slot: int) -> None:
+        """exec with per-pass CUDA events recorded in timing slot `slot` (no sync)."""
+        _check(lib().nufft_plan2_exec_timed(self._h, c_ptr, f_ptr, stream or None, slot))
+
+    def timing_read(self, nslots: int):
+        """(ms_pass1_total, ms_pass2_total) over slots [0, nslots)."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().nufft_plan2_timing_read(self._h, nslots, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def execute_host_ptr(self, c_ptr: int, f_ptr: int, batch: int = 1) -> None:
+        """exec through the host-pointer C-ABI call (copies inside)."""
+        _check(lib().nufft_plan2_exec_host(self._h, c_ptr, self.size(), f_ptr, batch))
+
+    def adjoint(self, f) -> np.ndarray:
+        f = _c128(f)
+        out = np.empty_like(f)
+        _check(lib().nufft_plan2_adjoint_host(self._h, _ptr(f), len(f), _ptr(out)))
+        return out
+
+
+class Plan1(_PlanBase):
+    """Type-I plan (transforms.hpp:237-244)."""
+    _kind = "plan1"
+
+    def __init__(self, handle, freqs):
+        super().__init__(handle)
+        self.freqs = freqs
+
+    def rank(self) -> int:
+        return self._info.rank
+
+    def gamma(self) -> float:
+        return self._info.gamma
+
+    def execute(self, c) -> np.ndarray:
+        c = _c128(c)
+        batch = 1 if c.ndim == 1 else c.shape[0]
+        f = np.empty_like(c)
+        _check(lib().nufft_plan1_exec_host(self._h, _ptr(c), c.shape[-1], _ptr(f), batch))
+        return f
+
+    def execute_device(self, c_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
+        _check(lib().nufft_plan1_exec(self._h, c_ptr, f_ptr, batch, stream or None))
+
+
+class Plan3(_PlanBase):
+    """Type-III plan (transforms.hpp:308-319)."""
+    _kind = "plan3"
+
+    @property
+    def bTrivial(self) -> bool:  # noqa: N802 (reference member name)
+        return bool(self._info.btrivial)
+
+    def effective_rank(self) -> int:
+        return self._info.effective_rank
+
+    @property
+    def rank_a(self) -> int:
+        return self._info.rank
+
+    @property
+    def rank_inner(self) -> int:
+        return self._info.rank2
+
+    def execute(self, c) -> np.ndarray:
+        c = _c128(c)
+        batch = 1 if c.ndim == 1 else c.shape[0]
+        f = np.empty_like(c)
+        _check(lib().nufft_plan3_exec_host(self._h, _ptr(c), c.shape[-1], _ptr(f), batch))
+        return f
+
+    def execute_device(self, c_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
+        _check(lib().nufft_plan3_exec(self._h, c_ptr, f_ptr, batch, stream or None))
+
+
+class Plan2D(_PlanBase):
+    """2D type-II plan (transform2d.hpp:51-59)."""
+    _kind = "plan2d2"
+
+    @property
+    def m(self) -> int:
+        return self._info.m
+
+    @property
+    def n(self) -> int:
+        return self._info.ncols
+
+    def rank_x(self) -> int:
+        return self._info.rank
+
+    def rank_y(self) -> int:
+        return self._info.rank2
+
+    def grid(self):
+        c = self.size()
+        arrs = [np.zeros(c), np.zeros(c), np.zeros(c, np.int64), np.zeros(c, np.int64),
+                np.zeros(c, np.uint64), np.zeros(c, np.uint64), np.zeros(c, np.uint64)]
+        _check(lib().nufft_plan2d2_samples(self._h, *[_ptr(a) for a in arrs]))
+        keys = ["x", "y", "sx", "sy", "tx", "ty", "flatIndex"]
+        out = dict(zip(keys, arrs))
+        out["gammaX"], out["gammaY"] = self._info.gamma, self._info.gamma2
+        return out
+
+    def execute(self, C2, reuse_row_stage: bool = True) -> np.ndarray:
+        C2 = _c128(C2)
+        if C2.ndim != 2:
+            raise InvalidArgument("exec_nufft2d2: coefficient dimensions mismatch")
+        f = np.empty(self.size(), np.complex128)
+        _check(lib().nufft_plan2d2_exec_host_impl(self._h, _ptr(C2), C2.shape[0], C2.shape[1],
+                                                  _ptr(f), 1, 1 if reuse_row_stage else 0))
+        return f
+
+    def execute_device(self, C_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
+        _check(lib().nufft_plan2d2_exec(self._h, C_ptr, f_ptr, batch, stream or None))
+
+
+def plan_nufft2(x_raw, epsilon: float, device: int = -1) -> Plan2:
+    x = _f64(x_raw)
+    h = C.c_void_p()
+    _check(lib().nufft_plan2_create(_ptr(x), len(x), epsilon, device, C.byref(h)))
+    return Plan2(h)
+
+
+def plan_nufft2_device(x_ptr: int, n: int, epsilon: float, device: int = -1) -> Plan2:
+    h = C.c_void_p()
+    _check(lib().nufft_plan2_create_device(x_ptr, n, epsilon, device, C.byref(h)))
+    return Plan2(h)
+
+
+def exec_nufft2(plan: Plan2, c, threads: int = 1) -> np.ndarray:
+    return plan.execute(c, threads)
+
+
+def exec_nufft2_adjoint(plan: Plan2, f) -> np.ndarray:
+    return plan.adjoint(f)
+
+
+def plan_nufft1(omega, epsilon: float, device: int = -1) -> Plan1:
+    w = _f64(omega)
+    h = C.c_void_p()
+    _check(lib().nufft_plan1_create(_ptr(w), len(w), epsilon, device, C.byref(h)))
+    return Plan1(h, w.copy())
+
+
+def exec_nufft1(plan: Plan1, c) -> np.ndarray:
+    return plan.execute(c)
+
+
+def plan_nufft3(x_raw, omega, epsilon: float, device: int = -1) -> Plan3:
+    x, w = _f64(x_raw), _f64(omega)
+    h = C.c_void_p()
+    _check(lib().nufft_plan3_create(_ptr(x), _ptr(w), len(x), len(w), epsilon, device, C.byref(h)))
+    return Plan3(h)
+
+
+def exec_nufft3(plan: Plan3, c) -> np.ndarray:
+    return plan.execute(c)
+
+
+def plan_nufft2d2(x_raw, y_raw, m: int, n: int, epsilon: float, device: int = -1) -> Plan2D:
+    x, y = _f64(x_raw), _f64(y_raw)
+    h = C.c_void_p()
+    _check(lib().nufft_plan2d2_create(_ptr(x), _ptr(y), len(x), len(y), m, n, epsilon, device,
+                                      C.byref(h)))
+    return Plan2D(h)
+
+
+def exec_nufft2d2(plan: Plan2D, C2) -> np.ndarray:
+    return plan.execute(C2, True)
+
+
+def exec_nufft2d2_impl(plan: Plan2D, C2, reuse_row_stage: bool) -> np.ndarray:
+    return plan.execute(C2, reuse_row_stage)

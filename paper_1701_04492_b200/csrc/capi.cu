@@ -1,0 +1,765 @@
+// C-ABI of the B200 low-rank NUFFT (include/nufft_b200.h).
+//
+// Validation order and messages follow the reference so the C++ layer can
+// re-throw the same exception types at the same points:
+//   plan_nufft2 transforms.hpp:133-147, plan_nufft1 :246-285,
+//   plan_nufft3 :321-380, plan_nufft2d2 transform2d.hpp:65-100,
+//   exec length checks :171, :208, :384, transform2d.hpp:109-110.
+#include <array>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/nufft_b200.h"
+#include "lowrank_host.hpp"
+#include "plans.hpp"
+
+struct nufft_plan2 {
+    nb::CorePlan core;
+    // per-pass timing events for the benchmark (exec_timed / timing_read)
+    mutable std::mutex timing_mu;
+    mutable std::vector<std::array<cudaEvent_t, 3>> timing;
+    ~nufft_plan2() {
+        for (auto& e : timing)
+            for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+struct nufft_plan1 {
+    nb::CorePlan core;
+};
+struct nufft_plan3 {
+    nb::Plan3State st;
+};
+struct nufft_plan2d {
+    nb::Plan2DState st;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return NUFFT_OK;
+    } catch (const nb::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("host allocation failed: ") + e.what();
+        return NUFFT_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NUFFT_INTERNAL;
+    }
+}
+
+cudaStream_t as_stream(void* s) { return s ? static_cast<cudaStream_t>(s) : cudaStreamPerThread; }
+
+int pick_device(int device) {
+    int count = 0;
+    NB_CUDA(cudaGetDeviceCount(&count));
+    if (count == 0) throw nb::Error(nb::kCudaError, "no CUDA device");
+    if (device < 0) NB_CUDA(cudaGetDevice(&device));
+    if (device >= count) nb::throw_invalid("device index out of range");
+    NB_CUDA(cudaSetDevice(device));
+    nb::DeviceCtx::get(device);
+    return device;
+}
+
+void check_epsilon(double eps) {  // transforms.hpp:118-121
+    if (!(eps > 0.0) || !(eps < 1.0)) nb::throw_domain("epsilon must be in (0, 1)");
+}
+void check_size(size_t n) {
+    if (n >= (size_t(1) << 31)) nb::throw_invalid("transform size exceeds 2^31 - 1 samples");
+}
+
+inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+__global__ void k_scale(double2* v, long long n, double s) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = make_double2(v[i].x * s, v[i].y * s);
+}
+__global__ void k_any_wrap(const long long* s, const long long* t, long long n, int* flag) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && s[i] != t[i]) atomicOr(flag, 1);
+}
+__global__ void k_flat_index(const long long* tx, const long long* ty, long long count, long long m,
+                             long long* flat) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < count) flat[j] = m * tx[j] + ty[j];
+}
+__global__ void k_omega_scaled(double* w, long long n) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < n) w[k] = (double)k / (double)n;
+}
+__global__ void k_fill_ones(double2* u, long long n) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < n) u[k] = make_double2(1.0, 0.0);
+}
+
+template <class T>
+void d2h(T* dst, const nb::DevArray& src, size_t count, cudaStream_t s) {
+    NB_CUDA(cudaMemcpyAsync(dst, src.as<T>(), sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+}
+
+// host -> device -> op -> host with stream-ordered scratch
+template <class Op>
+void host_roundtrip(const double* in, size_t in_doubles, double* out, size_t out_doubles,
+                    cudaStream_t s, Op op) {
+    nb::DevBuf din(8 * in_doubles, s), dout(8 * out_doubles, s);
+    NB_CUDA(cudaMemcpyAsync(din.get(), in, 8 * in_doubles, cudaMemcpyHostToDevice, s));
+    op(din.as<double2>(), dout.as<double2>());
+    NB_CUDA(cudaMemcpyAsync(out, dout.get(), 8 * out_doubles, cudaMemcpyDeviceToHost, s));
+    NB_CUDA(cudaStreamSynchronize(s));
+}
+
+void materialize_u(const nb::CorePlan& p, double2* u_dev, cudaStream_t s) {
+    if (p.uniform) {
+        k_fill_ones<<<blocks(p.n), 256, 0, s>>>(u_dev, (long long)p.n);
+        NB_LAUNCH();
+    } else {
+        nb::factors_u(p.ax.delta.as<double>(), p.n, p.gamma_factors, p.K, u_dev, s);
+    }
+}
+void materialize_v(const nb::CorePlan& p, double2* v_dev, cudaStream_t s) {
+    if (p.uniform) {
+        k_fill_ones<<<blocks(p.n), 256, 0, s>>>(v_dev, (long long)p.n);
+        NB_LAUNCH();
+        return;
+    }
+    nb::DevBuf w(8 * p.n, s);
+    k_omega_scaled<<<blocks(p.n), 256, 0, s>>>(w.as<double>(), (long long)p.n);
+    NB_LAUNCH();
+    nb::factors_v(w.as<double>(), p.n, p.K, v_dev, s);
+}
+
+void core_samples(const nb::CorePlan& p, double* x, long* sv, size_t* t) {
+    cudaStream_t s = cudaStreamPerThread;
+    NB_CUDA(cudaSetDevice(p.device));
+    if (x) d2h(x, p.ax.x, p.n, s);
+    static_assert(sizeof(long) == 8 && sizeof(size_t) == 8, "LP64");
+    if (sv) d2h(reinterpret_cast<long long*>(sv), p.ax.s, p.n, s);
+    if (t) d2h(reinterpret_cast<long long*>(t), p.ax.t, p.n, s);
+    NB_CUDA(cudaStreamSynchronize(s));
+}
+
+void fill_info(const nb::CorePlan& p, nufft_plan_info* info) {
+    std::memset(info, 0, sizeof(*info));
+    info->n = p.n;
+    info->rank = p.K;
+    info->rank2 = p.K;
+    info->effective_rank = p.K;
+    info->gamma = p.ax.gamma;
+    info->epsilon = p.epsilon;
+    info->btrivial = 1;
+    info->device = p.device;
+    info->path = p.fused ? 1 : 0;
+}
+
+// fft.hpp:161-178 on the device: rows contiguous; columns via transpose
+void rows_fft(double2* d, size_t rows, size_t cols, cudaStream_t s, int dev) {
+    nb::fft_exec(d, d, cols, rows, -1, s, dev);
+    nb::fft_count(cols, rows);
+}
+void cols_fft(double2* d, size_t rows, size_t cols, cudaStream_t s, int dev) {
+    nb::DevBuf tmp(sizeof(double2) * rows * cols, s);
+    nb::transpose(d, tmp.as<double2>(), rows, cols, 1, s);
+    nb::fft_exec(tmp.as<double2>(), tmp.as<double2>(), rows, cols, -1, s, dev);
+    nb::fft_count(rows, cols);
+    nb::transpose(tmp.as<double2>(), d, cols, rows, 1, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nufft_last_error(void) { return g_err.c_str(); }
+int nufft_abi_version(void) { return NUFFT_B200_ABI_VERSION; }
+int nufft_device_count(int* count) {
+    return guard([&] {
+        int c = 0;
+        cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+// ------------------------------------------------------------ special/lowrank
+int nufft_lambert_w(double x, double* out) {
+    return guard([&] { *out = nb::lambert_w(x); });
+}
+int nufft_bessel_j_int(int order, double z, double* out) {
+    return guard([&] { *out = nb::bessel_j_int(order, z); });
+}
+int nufft_bessel_j_signed(int order, double z, double* out) {
+    return guard([&] { *out = nb::bessel_j_signed(order, z); });
+}
+int nufft_select_rank(double gamma, double epsilon, size_t* rank) {
+    return guard([&] { *rank = nb::select_rank(gamma, epsilon); });
+}
+int nufft_cheb_coefficients(double gamma, size_t K, double* a) {
+    return guard([&] {
+        auto v = nb::cheb_coefficients(gamma, K);
+        std::memcpy(a, v.data(), 8 * v.size());
+    });
+}
+int nufft_cheb_eval_matrix(const double* points, size_t n, size_t K, double* out) {
+    return guard([&] {
+        if (K < 1) nb::throw_invalid("cheb_eval_matrix: K must be >= 1");
+        const int dev = pick_device(-1);
+        (void)dev;
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf din(8 * n, s), dout(8 * n * K, s);
+        if (n) NB_CUDA(cudaMemcpyAsync(din.get(), points, 8 * n, cudaMemcpyHostToDevice, s));
+        nb::cheb_eval(din.as<double>(), n, K, dout.as<double>(), s);
+        if (n) NB_CUDA(cudaMemcpyAsync(out, dout.get(), 8 * n * K, cudaMemcpyDeviceToHost, s));
+        NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int nufft_build_factors(const double* delta, size_t n, double gamma, const double* omega_scaled,
+                        size_t m, double epsilon, size_t* rank, double* u, double* v) {
+    return guard([&] {
+        if (gamma == 0.0) {  // lowrank.hpp:167-172
+            *rank = 1;
+            for (size_t j = 0; u && j < n; ++j) u[2 * j] = 1.0, u[2 * j + 1] = 0.0;
+            for (size_t k = 0; v && k < m; ++k) v[2 * k] = 1.0, v[2 * k + 1] = 0.0;
+            return;
+        }
+        const size_t K = nb::select_rank(gamma, epsilon);
+        *rank = K;
+        if (!u && !v) return;
+        pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        if (u) {
+            nb::DevBuf dd(8 * n, s), du(16 * n * K, s);
+            if (n) NB_CUDA(cudaMemcpyAsync(dd.get(), delta, 8 * n, cudaMemcpyHostToDevice, s));
+            if (n) nb::factors_u(dd.as<double>(), n, gamma, K, du.as<double2>(), s);
+            else (void)nb::cheb_coefficients(gamma, K + nb::kCoefficientPadding);
+            if (n) NB_CUDA(cudaMemcpyAsync(u, du.get(), 16 * n * K, cudaMemcpyDeviceToHost, s));
+            NB_CUDA(cudaStreamSynchronize(s));
+        }
+        if (v) {
+            nb::DevBuf dw(8 * m, s), dv(16 * m * K, s);
+            if (m) NB_CUDA(cudaMemcpyAsync(dw.get(), omega_scaled, 8 * m, cudaMemcpyHostToDevice, s));
+            if (m) nb::factors_v(dw.as<double>(), m, K, dv.as<double2>(), s);
+            if (m) NB_CUDA(cudaMemcpyAsync(v, dv.get(), 16 * m * K, cudaMemcpyDeviceToHost, s));
+            NB_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+// ------------------------------------------------------------ fft
+int nufft_fft_forward_host(const double* in, double* out, size_t n) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("fft_forward: empty input");
+        const int dev = pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(in, 2 * n, out, 2 * n, s, [&](double2* a, double2* b) {
+            nb::fft_exec(a, b, n, 1, -1, s, dev);
+            nb::fft_count(n);
+        });
+    });
+}
+int nufft_fft_inverse_host(const double* in, double* out, size_t n) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("fft_inverse: empty input");
+        const int dev = pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(in, 2 * n, out, 2 * n, s, [&](double2* a, double2* b) {
+            nb::fft_exec(a, b, n, 1, +1, s, dev);
+            nb::fft_count(n);
+            k_scale<<<blocks(n), 256, 0, s>>>(b, (long long)n, 1.0 / (double)n);
+            NB_LAUNCH();
+        });
+    });
+}
+int nufft_fft_2d_forward_host(const double* in, double* out, size_t rows, size_t cols) {
+    return guard([&] {
+        if (rows * cols == 0) nb::throw_invalid("fft_2d_forward: empty input");
+        const int dev = pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(in, 2 * rows * cols, out, 2 * rows * cols, s, [&](double2* a, double2* b) {
+            NB_CUDA(cudaMemcpyAsync(b, a, 16 * rows * cols, cudaMemcpyDeviceToDevice, s));
+            cols_fft(b, rows, cols, s, dev);
+            rows_fft(b, rows, cols, s, dev);
+        });
+    });
+}
+int nufft_fft_cols_forward_host(double* inout, size_t rows, size_t cols) {
+    return guard([&] {
+        if (rows * cols == 0) return;
+        const int dev = pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(inout, 2 * rows * cols, inout, 2 * rows * cols, s,
+                       [&](double2* a, double2* b) {
+                           NB_CUDA(cudaMemcpyAsync(b, a, 16 * rows * cols, cudaMemcpyDeviceToDevice, s));
+                           cols_fft(b, rows, cols, s, dev);
+                       });
+    });
+}
+int nufft_fft_rows_forward_host(double* inout, size_t rows, size_t cols) {
+    return guard([&] {
+        if (rows * cols == 0) return;
+        const int dev = pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(inout, 2 * rows * cols, inout, 2 * rows * cols, s,
+                       [&](double2* a, double2* b) {
+                           NB_CUDA(cudaMemcpyAsync(b, a, 16 * rows * cols, cudaMemcpyDeviceToDevice, s));
+                           rows_fft(b, rows, cols, s, dev);
+                       });
+    });
+}
+int nufft_fft_exec(const double* in_dev, double* out_dev, size_t n, size_t batch, int sign,
+                   void* stream) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("fft: empty input");
+        int dev;
+        NB_CUDA(cudaGetDevice(&dev));
+        nb::fft_exec(reinterpret_cast<const double2*>(in_dev), reinterpret_cast<double2*>(out_dev),
+                     n, batch, sign < 0 ? -1 : +1, as_stream(stream), dev);
+        nb::fft_count(n, batch);
+    });
+}
+uint64_t nufft_fft_exec_count(size_t n) { return nb::fft_exec_count(n); }
+uint64_t nufft_kernel_launch_count(void) { return nb::launch_count(); }
+void nufft_fft_reset_exec_counts(void) { nb::fft_reset_exec_counts(); }
+
+// ------------------------------------------------------------ samples
+int nufft_normalize_samples(const double* raw, size_t n, double* out) {
+    return guard([&] {
+        pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        if (n == 0) return;
+        nb::Axis ax;
+        nb::assign_samples(ax, raw, false, n, 1, s);
+        d2h(out, ax.x, n, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int nufft_grid_assign(const double* x, size_t n, size_t grid, long* sv, size_t* t, double* gamma) {
+    return guard([&] {
+        if (grid < 1) nb::throw_invalid("grid_assign: grid size must be >= 1");
+        pick_device(-1);
+        cudaStream_t s = cudaStreamPerThread;
+        if (n == 0) {
+            *gamma = 0.0;
+            return;
+        }
+        nb::Axis ax;
+        nb::assign_samples(ax, x, false, n, grid, s);
+        d2h(reinterpret_cast<long long*>(sv), ax.s, n, s);
+        d2h(reinterpret_cast<long long*>(t), ax.t, n, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *gamma = ax.gamma;
+    });
+}
+
+// ------------------------------------------------------------ type II
+static int plan2_create_impl(const double* x, bool on_dev, size_t n, double eps, int device,
+                             nufft_plan2** out) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("plan_nufft2: no samples");
+        check_epsilon(eps);
+        check_size(n);
+        const int dev = pick_device(device);
+        auto p = std::make_unique<nufft_plan2>();
+        nb::CorePlan& c = p->core;
+        c.device = dev;
+        c.n = n;
+        c.epsilon = eps;
+        cudaStream_t s = cudaStreamPerThread;
+        nb::assign_samples(c.ax, x, on_dev, n, n, s);
+        nb::finish_core(c, c.ax.gamma, s);
+        nb::build_bins(c, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = p.release();
+    });
+}
+int nufft_plan2_create(const double* x_raw, size_t n, double epsilon, int device, nufft_plan2** out) {
+    return plan2_create_impl(x_raw, false, n, epsilon, device, out);
+}
+int nufft_plan2_create_device(const double* x_raw_dev, size_t n, double epsilon, int device,
+                              nufft_plan2** out) {
+    return plan2_create_impl(x_raw_dev, true, n, epsilon, device, out);
+}
+void nufft_plan2_destroy(nufft_plan2* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->core.device);
+    cudaDeviceSynchronize();
+    delete plan;
+}
+int nufft_plan2_info(const nufft_plan2* plan, nufft_plan_info* info) {
+    return guard([&] { fill_info(plan->core, info); });
+}
+int nufft_plan2_samples(const nufft_plan2* plan, double* x, long* s, size_t* t) {
+    return guard([&] { core_samples(plan->core, x, s, t); });
+}
+int nufft_plan2_factors(const nufft_plan2* plan, double* u, double* v) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf d(16 * p.n * p.K, s);
+        if (u) {
+            materialize_u(p, d.as<double2>(), s);
+            NB_CUDA(cudaMemcpyAsync(u, d.get(), 16 * p.n * p.K, cudaMemcpyDeviceToHost, s));
+            NB_CUDA(cudaStreamSynchronize(s));
+        }
+        if (v) {
+            materialize_v(p, d.as<double2>(), s);
+            NB_CUDA(cudaMemcpyAsync(v, d.get(), 16 * p.n * p.K, cudaMemcpyDeviceToHost, s));
+            NB_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+int nufft_plan2_exec_terms(const nufft_plan2* plan, const double* c_dev, double* f_dev,
+                           size_t batch, size_t r_begin, size_t r_end, void* stream) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        if (r_end > p.K) r_end = p.K;
+        nb::exec_type2(p, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev),
+                       batch, r_begin, r_end, as_stream(stream));
+        if (r_end > r_begin) nb::fft_count(p.n, (r_end - r_begin) * batch);
+    });
+}
+int nufft_plan2_exec_timed(const nufft_plan2* plan, const double* c_dev, double* f_dev,
+                           void* stream, int slot) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        if (!p.fused) nb::throw_invalid("exec_timed: plan does not use the fused two-pass path");
+        cudaEvent_t* ev = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(plan->timing_mu);
+            while ((int)plan->timing.size() <= slot) {
+                std::array<cudaEvent_t, 3> e{};
+                for (auto& x : e) NB_CUDA(cudaEventCreate(&x));
+                plan->timing.push_back(e);
+            }
+            ev = plan->timing[slot].data();
+        }
+        nb::exec_type2(p, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev),
+                       1, 0, p.K, as_stream(stream), ev);
+        nb::fft_count(p.n, p.K);
+    });
+}
+int nufft_plan2_timing_read(const nufft_plan2* plan, int nslots, double* ms_pass1,
+                            double* ms_pass2) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lock(plan->timing_mu);
+        if (nslots > (int)plan->timing.size()) nb::throw_invalid("timing_read: slot out of range");
+        double a = 0, b = 0;
+        for (int i = 0; i < nslots; ++i) {
+            auto& e = plan->timing[i];
+            NB_CUDA(cudaEventSynchronize(e[2]));
+            float t1 = 0, t2 = 0;
+            NB_CUDA(cudaEventElapsedTime(&t1, e[0], e[1]));
+            NB_CUDA(cudaEventElapsedTime(&t2, e[1], e[2]));
+            a += t1;
+            b += t2;
+        }
+        *ms_pass1 = a;
+        *ms_pass2 = b;
+    });
+}
+int nufft_plan2_exec(const nufft_plan2* plan, const double* c_dev, double* f_dev, size_t batch,
+                     void* stream) {
+    return nufft_plan2_exec_terms(plan, c_dev, f_dev, batch, 0, plan->core.K, stream);
+}
+int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, double* f,
+                          size_t batch) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("exec_nufft2: length mismatch");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(c, 2 * p.n * batch, f, 2 * p.n * batch, s, [&](double2* a, double2* b) {
+            nb::exec_type2(p, a, b, batch, 0, p.K, s);
+            nb::fft_count(p.n, p.K * batch);
+        });
+    });
+}
+static void adjoint_dev(const nb::CorePlan& p, const double2* fin, double2* out, cudaStream_t s) {
+    nb::DevBuf g(16 * p.n, s);
+    nb::conj_copy(fin, g.as<double2>(), p.n, s);
+    nb::exec_transpose(p, g.as<double2>(), out, 1, s);
+    nb::conj_copy(out, out, p.n, s);
+    nb::fft_count(p.n, p.K);
+}
+int nufft_plan2_adjoint(const nufft_plan2* plan, const double* f_dev, double* out_dev, void* stream) {
+    return guard([&] {
+        NB_CUDA(cudaSetDevice(plan->core.device));
+        adjoint_dev(plan->core, reinterpret_cast<const double2*>(f_dev),
+                    reinterpret_cast<double2*>(out_dev), as_stream(stream));
+    });
+}
+int nufft_plan2_adjoint_host(const nufft_plan2* plan, const double* f, size_t len, double* out) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("nufft transpose: length mismatch");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(f, 2 * p.n, out, 2 * p.n, s,
+                       [&](double2* a, double2* b) { adjoint_dev(p, a, b, s); });
+    });
+}
+
+// ------------------------------------------------------------ type I
+int nufft_plan1_create(const double* omega, size_t n, double epsilon, int device, nufft_plan1** out) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("plan_nufft1: no frequencies");
+        check_epsilon(epsilon);
+        check_size(n);
+        const int dev = pick_device(device);
+        auto p = std::make_unique<nufft_plan1>();
+        nb::CorePlan& c = p->core;
+        c.device = dev;
+        c.n = n;
+        c.epsilon = epsilon;
+        cudaStream_t s = cudaStreamPerThread;
+        nb::assign_frequencies(c.ax, omega, false, n, false, s);
+        nb::finish_core(c, c.ax.gamma_raw, s);  // un-snapped gamma, transforms.hpp:282
+        nb::build_bins(c, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = p.release();
+    });
+}
+void nufft_plan1_destroy(nufft_plan1* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->core.device);
+    cudaDeviceSynchronize();
+    delete plan;
+}
+int nufft_plan1_info(const nufft_plan1* plan, nufft_plan_info* info) {
+    return guard([&] { fill_info(plan->core, info); });
+}
+int nufft_plan1_samples(const nufft_plan1* plan, double* x, long* s, size_t* t) {
+    return guard([&] { core_samples(plan->core, x, s, t); });
+}
+int nufft_plan1_exec(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
+                     void* stream) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        nb::exec_transpose(p, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev),
+                           batch, as_stream(stream));
+        nb::fft_count(p.n, p.K * batch);
+    });
+}
+int nufft_plan1_exec_host(const nufft_plan1* plan, const double* c, size_t len, double* f,
+                          size_t batch) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("nufft transpose: length mismatch");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(c, 2 * p.n * batch, f, 2 * p.n * batch, s, [&](double2* a, double2* b) {
+            nb::exec_transpose(p, a, b, batch, s);
+            nb::fft_count(p.n, p.K * batch);
+        });
+    });
+}
+
+// ------------------------------------------------------------ type III
+int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, size_t n_omega,
+                       double epsilon, int device, nufft_plan3** out) {
+    return guard([&] {
+        if (n_x != n_omega) nb::throw_invalid("plan_nufft3: sample/frequency length mismatch");
+        if (n_x == 0) nb::throw_invalid("plan_nufft3: no samples");
+        check_epsilon(epsilon);
+        check_size(n_x);
+        const size_t n = n_x;
+        const int dev = pick_device(device);
+        auto p = std::make_unique<nufft_plan3>();
+        nb::Plan3State& st = p->st;
+        cudaStream_t s = cudaStreamPerThread;
+        // frequencies first (transforms.hpp:329-331 validates them before the samples)
+        st.inner.device = dev;
+        st.inner.n = n;
+        st.inner.epsilon = epsilon;
+        nb::assign_frequencies(st.inner.ax, omega, false, n, true, s);
+        st.a.device = dev;
+        st.a.n = n;
+        st.a.epsilon = epsilon;
+        nb::assign_samples(st.a.ax, x_raw, false, n, n, s);
+        st.omega.alloc(8 * n);
+        NB_CUDA(cudaMemcpyAsync(st.omega.as<double>(), omega, 8 * n, cudaMemcpyHostToDevice, s));
+        // factors A: gamma = samples.gamma (snapped), v over omega/N (transforms.hpp:337-340)
+        st.a.gamma_factors = st.a.ax.gamma;
+        st.a.uniform = st.a.gamma_factors == 0.0;
+        st.a.K = st.a.uniform ? 1 : nb::select_rank(st.a.gamma_factors, epsilon);
+        st.a.series_deg = nb::bessel_series_degrees(st.a.gamma_factors, st.a.K);
+        nb::DevBuf flag(4, s);
+        NB_CUDA(cudaMemsetAsync(flag.get(), 0, 4, s));
+        k_any_wrap<<<blocks(n), 256, 0, s>>>(st.a.ax.s.as<long long>(), st.a.ax.t.as<long long>(),
+                                             (long long)n, flag.as<int>());
+        NB_LAUNCH();
+        int wrap = 0;
+        NB_CUDA(cudaMemcpyAsync(&wrap, flag.get(), 4, cudaMemcpyDeviceToHost, s));
+        NB_CUDA(cudaStreamSynchronize(s));
+        st.btrivial = wrap == 0;
+        st.kc = st.btrivial ? st.a.K : 2 * st.a.K;
+        // inner type-I plan on omega (transforms.hpp:378)
+        nb::finish_core(st.inner, st.inner.ax.gamma_raw, s);
+        nb::build_bins(st.inner, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = p.release();
+    });
+}
+void nufft_plan3_destroy(nufft_plan3* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->st.a.device);
+    cudaDeviceSynchronize();
+    delete plan;
+}
+int nufft_plan3_info(const nufft_plan3* plan, nufft_plan_info* info) {
+    return guard([&] {
+        const nb::Plan3State& st = plan->st;
+        fill_info(st.a, info);
+        info->rank = st.a.K;
+        info->rank2 = st.inner.K;
+        info->effective_rank = st.kc;
+        info->gamma = st.a.ax.gamma;
+        info->gamma2 = st.inner.ax.gamma;
+        info->btrivial = st.btrivial ? 1 : 0;
+        info->path = 0;
+    });
+}
+int nufft_plan3_samples(const nufft_plan3* plan, double* x, long* s, size_t* t) {
+    return guard([&] { core_samples(plan->st.a, x, s, t); });
+}
+int nufft_plan3_exec(const nufft_plan3* plan, const double* c_dev, double* f_dev, size_t batch,
+                     void* stream) {
+    return guard([&] {
+        const nb::Plan3State& st = plan->st;
+        NB_CUDA(cudaSetDevice(st.a.device));
+        nb::exec_type3(st, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev),
+                       batch, as_stream(stream));
+        nb::fft_count(st.a.n, st.kc * st.inner.K * batch);
+    });
+}
+int nufft_plan3_exec_host(const nufft_plan3* plan, const double* c, size_t len, double* f,
+                          size_t batch) {
+    return guard([&] {
+        const nb::Plan3State& st = plan->st;
+        if (len != st.a.n) nb::throw_invalid("exec_nufft3: length mismatch");
+        NB_CUDA(cudaSetDevice(st.a.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(c, 2 * st.a.n * batch, f, 2 * st.a.n * batch, s, [&](double2* a, double2* b) {
+            nb::exec_type3(st, a, b, batch, s);
+            nb::fft_count(st.a.n, st.kc * st.inner.K * batch);
+        });
+    });
+}
+
+// ------------------------------------------------------------ 2D type II
+int nufft_plan2d2_create(const double* x_raw, const double* y_raw, size_t count_x, size_t count_y,
+                         size_t m, size_t n, double epsilon, int device, nufft_plan2d** out) {
+    return guard([&] {
+        if (count_x == 0) nb::throw_invalid("plan_nufft2d2: no samples");
+        if (m < 1 || n < 1) nb::throw_invalid("plan_nufft2d2: grid sizes must be >= 1");
+        check_epsilon(epsilon);
+        check_size(count_x);
+        const int dev = pick_device(device);
+        auto p = std::make_unique<nufft_plan2d>();
+        nb::Plan2DState& st = p->st;
+        st.device = dev;
+        st.m = m;
+        st.n = n;
+        st.epsilon = epsilon;
+        cudaStream_t s = cudaStreamPerThread;
+        nb::assign_samples(st.ax, x_raw, false, count_x, n, s);
+        if (count_y) nb::assign_samples(st.ay, y_raw, false, count_y, m, s);
+        if (count_x != count_y) nb::throw_invalid("grid_assign_2d: coordinate length mismatch");
+        st.count = count_x;
+        st.ux_uniform = st.ax.gamma == 0.0;
+        st.uy_uniform = st.ay.gamma == 0.0;
+        st.kx = st.ux_uniform ? 1 : nb::select_rank(st.ax.gamma, epsilon);
+        st.ky = st.uy_uniform ? 1 : nb::select_rank(st.ay.gamma, epsilon);
+        st.deg_x = nb::bessel_series_degrees(st.ax.gamma, st.kx);
+        st.deg_y = nb::bessel_series_degrees(st.ay.gamma, st.ky);
+        st.flat.alloc(8 * st.count);
+        k_flat_index<<<blocks(st.count), 256, 0, s>>>(st.ax.t.as<long long>(), st.ay.t.as<long long>(),
+                                                      (long long)st.count, (long long)m,
+                                                      st.flat.as<long long>());
+        NB_LAUNCH();
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = p.release();
+    });
+}
+void nufft_plan2d2_destroy(nufft_plan2d* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->st.device);
+    cudaDeviceSynchronize();
+    delete plan;
+}
+int nufft_plan2d2_info(const nufft_plan2d* plan, nufft_plan_info* info) {
+    return guard([&] {
+        const nb::Plan2DState& st = plan->st;
+        std::memset(info, 0, sizeof(*info));
+        info->n = st.count;
+        info->rank = st.kx;
+        info->rank2 = st.ky;
+        info->effective_rank = st.kx * st.ky;
+        info->gamma = st.ax.gamma;
+        info->gamma2 = st.ay.gamma;
+        info->epsilon = st.epsilon;
+        info->btrivial = 1;
+        info->m = st.m;
+        info->ncols = st.n;
+        info->device = st.device;
+    });
+}
+int nufft_plan2d2_samples(const nufft_plan2d* plan, double* x, double* y, long* sx, long* sy,
+                          size_t* tx, size_t* ty, size_t* flat_index) {
+    return guard([&] {
+        const nb::Plan2DState& st = plan->st;
+        NB_CUDA(cudaSetDevice(st.device));
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t c = st.count;
+        if (x) d2h(x, st.ax.x, c, s);
+        if (y) d2h(y, st.ay.x, c, s);
+        if (sx) d2h(reinterpret_cast<long long*>(sx), st.ax.s, c, s);
+        if (sy) d2h(reinterpret_cast<long long*>(sy), st.ay.s, c, s);
+        if (tx) d2h(reinterpret_cast<long long*>(tx), st.ax.t, c, s);
+        if (ty) d2h(reinterpret_cast<long long*>(ty), st.ay.t, c, s);
+        if (flat_index) d2h(reinterpret_cast<long long*>(flat_index), st.flat, c, s);
+        NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int nufft_plan2d2_exec(const nufft_plan2d* plan, const double* C_dev, double* f_dev, size_t batch,
+                       void* stream) {
+    return guard([&] {
+        const nb::Plan2DState& st = plan->st;
+        NB_CUDA(cudaSetDevice(st.device));
+        nb::exec_2d(st, reinterpret_cast<const double2*>(C_dev), reinterpret_cast<double2*>(f_dev),
+                    batch, true, as_stream(stream));
+    });
+}
+int nufft_plan2d2_exec_host_impl(const nufft_plan2d* plan, const double* C, size_t rows,
+                                 size_t cols, double* f, size_t batch, int reuse_row_stage) {
+    return guard([&] {
+        const nb::Plan2DState& st = plan->st;
+        if (rows != st.m || cols != st.n)
+            nb::throw_invalid("exec_nufft2d2: coefficient dimensions mismatch");
+        NB_CUDA(cudaSetDevice(st.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(C, 2 * st.m * st.n * batch, f, 2 * st.count * batch, s,
+                       [&](double2* a, double2* b) { nb::exec_2d(st, a, b, batch, reuse_row_stage != 0, s); });
+    });
+}
+int nufft_plan2d2_exec_host(const nufft_plan2d* plan, const double* C, size_t rows, size_t cols,
+                            double* f, size_t batch) {
+    return nufft_plan2d2_exec_host_impl(plan, C, rows, cols, f, batch, 1);
+}
+
+}  // extern "C"

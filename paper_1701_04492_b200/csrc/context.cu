@@ -1,0 +1,104 @@
+// Per-device context, stream-ordered scratch, logical FFT counters.
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "engine.cuh"
+
+namespace nb {
+
+namespace {
+__global__ void k_twiddle_table(double2* tw, int L) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < L) tw[m] = unit_root(m, L);
+}
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DeviceCtx>> g_ctx;
+
+std::mutex g_count_mu;
+std::atomic<unsigned long long> g_launches{0};
+std::map<size_t, uint64_t> g_counts;
+}  // namespace
+
+void setup_mempool(int device) {
+    cudaMemPool_t pool;
+    NB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    NB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+}
+
+DeviceCtx& DeviceCtx::get(int device) {
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    auto it = g_ctx.find(device);
+    if (it != g_ctx.end()) return *it->second;
+    auto ctx = std::make_unique<DeviceCtx>();
+    ctx->device = device;
+    NB_CUDA(cudaSetDevice(device));
+    ctx->sms = sm_count(device);
+    setup_mempool(device);
+    for (int l = 1; l <= 12; ++l) {
+        const int L = 1 << l;
+        double2* p = nullptr;
+        NB_CUDA(cudaMalloc(&p, sizeof(double2) * L));
+        k_twiddle_table<<<(L + 255) / 256, 256>>>(p, L);
+        NB_LAUNCH();
+        ctx->tw[l] = p;
+    }
+    NB_CUDA(cudaDeviceSynchronize());
+    auto& ref = *ctx;
+    g_ctx.emplace(device, std::move(ctx));
+    return ref;
+}
+
+void DevBuf::alloc(size_t bytes, cudaStream_t s) {
+    release();
+    s_ = s;
+    if (bytes == 0) bytes = 16;
+    NB_CUDA(cudaMallocAsync(&p_, bytes, s));
+}
+void DevBuf::release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+}
+
+DevArray::~DevArray() {
+    if (p_) cudaFree(p_);
+}
+DevArray& DevArray::operator=(DevArray&& o) noexcept {
+    if (this != &o) {
+        if (p_) cudaFree(p_);
+        p_ = o.p_;
+        bytes_ = o.bytes_;
+        o.p_ = nullptr;
+        o.bytes_ = 0;
+    }
+    return *this;
+}
+void DevArray::alloc(size_t bytes) {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    bytes_ = bytes;
+    NB_CUDA(cudaMalloc(&p_, bytes ? bytes : 16));
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(); }
+
+void fft_count(size_t n, uint64_t times) {
+    std::lock_guard<std::mutex> lock(g_count_mu);
+    g_counts[n] += times;
+}
+uint64_t fft_exec_count(size_t n) {
+    std::lock_guard<std::mutex> lock(g_count_mu);
+    auto it = g_counts.find(n);
+    return it == g_counts.end() ? 0 : it->second;
+}
+void fft_reset_exec_counts() {
+    std::lock_guard<std::mutex> lock(g_count_mu);
+    g_counts.clear();
+}
+
+}  // namespace nb

@@ -1,0 +1,86 @@
+// Host-side engine interfaces shared by the transform implementations.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nb {
+
+// Per-device constants: forward twiddle tables tw_L[m] = exp(-2 pi i m/L) for
+// L = 2^l, l = 1..12 (consumed by the block FFT), created once per device.
+struct DeviceCtx {
+    int device = 0;
+    int sms = 0;
+    const double2* tw[13] = {};
+    static DeviceCtx& get(int device);
+    const double2* table(int L) const { return tw[ilog2(static_cast<size_t>(L))]; }
+};
+
+// RAII stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync on the
+// device's default memory pool, whose release threshold is raised so that
+// repeated executions reuse memory instead of re-allocating).
+class DevBuf {
+  public:
+    DevBuf() = default;
+    DevBuf(size_t bytes, cudaStream_t s) { alloc(bytes, s); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), s_(o.s_) { o.p_ = nullptr; }
+    void alloc(size_t bytes, cudaStream_t s);
+    void release();
+    template <class T>
+    T* as() const { return static_cast<T*>(p_); }
+    void* get() const { return p_; }
+
+  private:
+    void* p_ = nullptr;
+    cudaStream_t s_ = nullptr;
+};
+
+// Persistent device allocation (plan-owned buffers).
+class DevArray {
+  public:
+    DevArray() = default;
+    explicit DevArray(size_t bytes) { alloc(bytes); }
+    ~DevArray();
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr; }
+    DevArray& operator=(DevArray&& o) noexcept;
+    void alloc(size_t bytes);
+    template <class T>
+    T* as() const { return static_cast<T*>(p_); }
+    size_t bytes() const { return bytes_; }
+
+  private:
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+void setup_mempool(int device);
+
+// ---- logical FFT execution counters (fft.hpp:91-95,126-137 test hook) -----
+void fft_count(size_t n, uint64_t times = 1);
+uint64_t fft_exec_count(size_t n);
+void fft_reset_exec_counts();
+unsigned long long launch_count();
+
+// ---- generic uniform FFT engine (any n >= 1, batched, contiguous) --------
+// out may equal in.  sign -1 forward, +1 backward (unnormalized).  Does NOT
+// touch the logical counters (callers count logical transforms).
+void fft_exec(const double2* in, double2* out, size_t n, size_t batch, int sign, cudaStream_t s,
+              int device);
+// batched out-of-place transpose: in is batch x rows x cols, out batch x cols x rows
+void transpose(const double2* in, double2* out, size_t rows, size_t cols, size_t batch,
+               cudaStream_t s);
+
+}  // namespace nb

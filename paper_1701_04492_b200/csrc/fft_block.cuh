@@ -1,0 +1,218 @@
+// In-register radix butterflies and the shared-memory Stockham block FFT.
+//
+// This is the uniform-FFT building block that replaces the reference's FFTW
+// calls (proj/include/nufft/fft.hpp:97-109).  Convention (fft.hpp:2-5):
+//   forward  (SIGN = -1): X_k = sum_j x_j exp(-2*pi*i*j*k/L), unnormalized
+//   backward (SIGN = +1): X_k = sum_j x_j exp(+2*pi*i*j*k/L), unnormalized
+//
+// A group of G = L/16 threads computes one L-point transform (L = 16..4096,
+// power of two).  Thread `tid` holds v[q] = x[tid + q*G] (q < 16) on entry and
+// v[q] = X[tid + q*G] on exit — coalesced with unit stride across the group
+// on both sides, so prologues (loads + diagonal scaling) and epilogues fuse
+// directly onto the register arrays.  Stages are Stockham autosort with
+// radix 16 (and one final radix 8/4/2 stage when log2 L is not a multiple of
+// 4); between stages the data crosses shared memory once (write + read) in
+// a ping-pong pair of padded buffers, one barrier per exchange.
+#pragma once
+
+#include "common.cuh"
+
+namespace nb {
+
+// exp(SIGN*2*pi*i*Q/16) multiply, special-casing the quarter turns
+template <int Q, int SIGN>
+__device__ __forceinline__ double2 mul_w16(double2 a) {
+    constexpr int q = ((Q % 16) + 16) % 16;
+    if constexpr (q == 0) {
+        return a;
+    } else if constexpr (q == 8) {
+        return make_double2(-a.x, -a.y);
+    } else if constexpr (q == 4 || q == 12) {
+        // multiply by SIGN*i (q==4) or -SIGN*i (q==12)
+        constexpr int s = (q == 4) ? SIGN : -SIGN;
+        return s > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+    } else {
+        constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173,
+                         C2 = 0.70710678118654752440;
+        // cos/sin of 2*pi*q/16
+        constexpr double ctab[16] = {1, C1, C2, S1, 0, -S1, -C2, -C1, -1, -C1, -C2, -S1, 0, S1, C2, C1};
+        constexpr double stab[16] = {0, S1, C2, C1, 1, C1, C2, S1, 0, -S1, -C2, -C1, -1, -C1, -C2, -S1};
+        constexpr double c = ctab[q], s = SIGN * stab[q];
+        return make_double2(__fma_rn(a.x, c, -a.y * s), __fma_rn(a.x, s, a.y * c));
+    }
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft2(double2& a0, double2& a1) {
+    const double2 t = a0;
+    a0 = cadd(t, a1);
+    a1 = csub(t, a1);
+}
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+    const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+    const double2 s13 = cadd(a1, a3), d13 = csub(a1, a3);
+    const double2 w = mul_w16<4, SIGN>(d13);
+    a0 = cadd(s02, s13);
+    a2 = csub(s02, s13);
+    a1 = cadd(d02, w);
+    a3 = csub(d02, w);
+}
+
+// In-place R-point DFT of a[0..R-1] (natural order in and out), R in {2,4,8,16}.
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(double2* a) {
+    if constexpr (R == 1) {
+    } else if constexpr (R == 2) {
+        dft2<SIGN>(a[0], a[1]);
+    } else if constexpr (R == 4) {
+        dft4<SIGN>(a[0], a[1], a[2], a[3]);
+    } else if constexpr (R == 8) {
+        // t = t1 + 2*t2, k = k2 + 4*k1
+        dft4<SIGN>(a[0], a[2], a[4], a[6]);
+        dft4<SIGN>(a[1], a[3], a[5], a[7]);
+        a[3] = mul_w16<2, SIGN>(a[3]);
+        a[5] = mul_w16<4, SIGN>(a[5]);
+        a[7] = mul_w16<6, SIGN>(a[7]);
+        double2 o[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) {
+            double2 x0 = a[2 * k2], x1 = a[2 * k2 + 1];
+            dft2<SIGN>(x0, x1);
+            o[k2] = x0;
+            o[k2 + 4] = x1;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = o[i];
+    } else {
+        static_assert(R == 16, "radix");
+        // t = t1 + 4*t2 ; inner DFT4 over t2 for each t1 -> b[t1][k2] stored at a[t1 + 4*k2]
+        dft4<SIGN>(a[0], a[4], a[8], a[12]);
+        dft4<SIGN>(a[1], a[5], a[9], a[13]);
+        dft4<SIGN>(a[2], a[6], a[10], a[14]);
+        dft4<SIGN>(a[3], a[7], a[11], a[15]);
+        // twiddle w16^(t1*k2)
+        a[5] = mul_w16<1, SIGN>(a[5]);
+        a[9] = mul_w16<2, SIGN>(a[9]);
+        a[13] = mul_w16<3, SIGN>(a[13]);
+        a[6] = mul_w16<2, SIGN>(a[6]);
+        a[10] = mul_w16<4, SIGN>(a[10]);
+        a[14] = mul_w16<6, SIGN>(a[14]);
+        a[7] = mul_w16<3, SIGN>(a[7]);
+        a[11] = mul_w16<6, SIGN>(a[11]);
+        a[15] = mul_w16<9, SIGN>(a[15]);
+        // outer DFT4 over t1 for each k2 -> out[k2 + 4*k1]
+        dft4<SIGN>(a[0], a[1], a[2], a[3]);
+        dft4<SIGN>(a[4], a[5], a[6], a[7]);
+        dft4<SIGN>(a[8], a[9], a[10], a[11]);
+        dft4<SIGN>(a[12], a[13], a[14], a[15]);
+        // now a[4*k2 + k1] holds out[k2 + 4*k1]: transpose 4x4
+        double2 o[16];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2)
+#pragma unroll
+            for (int k1 = 0; k1 < 4; ++k1) o[k2 + 4 * k1] = a[4 * k2 + k1];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a[i] = o[i];
+    }
+}
+
+// padded shared-memory index: one 16-byte pad per 16 elements (bank spread)
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int L) { return L + L / 16; }
+
+// number of radix-16 stages and the remainder radix of an L-point FFT
+template <int L>
+struct FftShape {
+    static constexpr int LOG = ilog2_c(L);
+    static constexpr int N16 = LOG / 4;
+    static constexpr int REM = 1 << (LOG % 4);
+    static constexpr int STAGES = N16 + (REM > 1 ? 1 : 0);
+    static constexpr int G = L / 16;  // threads per transform
+    static_assert(L >= 16 && L <= 4096 && (1 << LOG) == L, "block FFT size");
+};
+
+// Twiddle exp(SIGN*2*pi*i*m/L) from the forward table tw (tw[m] = exp(-2*pi*i*m/L)).
+template <int SIGN>
+__device__ __forceinline__ double2 tw_fetch(const double2* __restrict__ tw, int m) {
+    const double2 w = __ldg(tw + m);
+    return SIGN < 0 ? w : make_double2(w.x, -w.y);
+}
+
+// One Stockham stage: radix R, Ns = product of the radices already applied.
+// Reads v (layout x[tid + q*G]); if !LAST writes the stage output to `out`
+// (padded, natural Stockham order); if LAST leaves it in v (same layout).
+template <int L, int R, int NS, bool LAST, int SIGN>
+__device__ __forceinline__ void stockham_stage(double2 (&v)[16], double2* out, int tid,
+                                               const double2* __restrict__ tw) {
+    constexpr int G = L / 16;
+    constexpr int B = 16 / R;  // butterflies per thread
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const int j = tid + b * G;
+        const int k = j & (NS - 1);
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = v[b + t * B];
+        if constexpr (NS > 1) {
+            constexpr int STEP = L / (NS * R);
+#pragma unroll
+            for (int t = 1; t < R; ++t) a[t] = cmul(a[t], tw_fetch<SIGN>(tw, k * t * STEP));
+        }
+        dft<R, SIGN>(a);
+        if constexpr (LAST) {
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[b + t * B] = a[t];
+        } else {
+            const int base = (j - k) * R + k;  // (j/Ns)*Ns*R + k
+#pragma unroll
+            for (int t = 0; t < R; ++t) out[pad16(base + t * NS)] = a[t];
+        }
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void load_stage_input(double2 (&v)[16], const double2* in, int tid) {
+    constexpr int G = L / 16;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = in[pad16(tid + q * G)];
+}
+
+// Full L-point FFT on the register array v (layout above).  buf0/buf1: two
+// padded shared buffers of padded_len(L) double2 owned by this group; `bar`
+// is the group barrier.  tw: forward table exp(-2*pi*i*m/L), m < L.
+// On exit the last-written buffer is buf[(STAGES-2)&1]; the other one is free.
+template <int L, int SIGN, class Bar>
+__device__ __forceinline__ void block_fft(double2 (&v)[16], double2* buf0, double2* buf1, int tid,
+                                          const double2* __restrict__ tw, Bar bar) {
+    using S = FftShape<L>;
+    constexpr int R_LAST = (S::REM > 1) ? S::REM : 16;
+    if constexpr (S::STAGES == 1) {
+        stockham_stage<L, 16, 1, true, SIGN>(v, nullptr, tid, tw);
+    } else if constexpr (S::STAGES == 2) {
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, tw);
+        bar();
+        load_stage_input<L>(v, buf0, tid);
+        stockham_stage<L, R_LAST, 16, true, SIGN>(v, nullptr, tid, tw);
+    } else if constexpr (S::STAGES == 3) {
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, tw);
+        bar();
+        load_stage_input<L>(v, buf0, tid);
+        stockham_stage<L, 16, 16, false, SIGN>(v, buf1, tid, tw);
+        bar();
+        load_stage_input<L>(v, buf1, tid);
+        stockham_stage<L, R_LAST, 256, true, SIGN>(v, nullptr, tid, tw);
+    } else {
+        static_assert(S::STAGES <= 3, "L <= 4096");
+    }
+}
+
+// the buffer that is NOT read by the final stage (safe to overwrite after
+// block_fft returns, once every thread of the group has passed the last barrier)
+template <int L>
+__device__ __forceinline__ double2* block_fft_free_buf(double2* buf0, double2* buf1) {
+    return (FftShape<L>::STAGES == 3) ? buf0 : buf1;
+}
+
+}  // namespace nb

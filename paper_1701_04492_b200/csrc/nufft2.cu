@@ -1,0 +1,470 @@
+// Type-II NUFFT execution — the north-star hot path.
+//
+// Reference: exec_nufft2 (proj/include/nufft/transforms.hpp:168-199) evaluates
+//   f = sum_{r<K} diag(u_r) I_N(t,:) F diag(v_r) c
+// as K separate passes of {scale, FFTW, gather} over HBM-sized vectors
+// (accumulate_term :152-161).  Here the K terms are fused into two passes of
+// a four-step FFT, N = N1 * N2 (k = k1*N2 + k2, t = t1 + N1*t2):
+//
+//  pass 1 (one CTA per column k2, persistent): the c column (N1 values) is
+//    read ONCE from HBM; for every r the v_r scaling (Chebyshev recurrence in
+//    registers) is applied on the fly, the N1-point column FFT runs in
+//    registers/shared memory, the inter-pass twiddle w_N^{t1 k2} is applied
+//    and Y_r[t1][k2] is written (the only HBM round trip of the K spectra).
+//  pass 2 (one CTA per row t1, persistent): for r = K-1 .. 0 the row Y_r[t1][:]
+//    is read, its N2-point FFT gives X_r[t1 + N1 t2] in shared memory, and every
+//    sample bucketed on this row (t_j mod N1 == t1, plan-time sort) gathers
+//    X_r[t2_j] into a per-sample register accumulator by Horner in r:
+//        acc <- acc * (i h_j) + g_r(h_j^2) X_r[t2_j]
+//    which sums u_r[j] X_r[t_j] over r without materializing u (Bessel form,
+//    bessel.cuh).  The scaled result 2 exp(2 i h_j) acc is written once to f[j].
+//
+// HBM bytes per point (batch 1): c 16 + f 16 + xs/perm 12 + 32 K (Y written
+// and read once) — SURVEY.md §8(d).  No atomics: every f[j] is owned by one
+// thread, and sums run in a fixed order, so results are bit-reproducible.
+#include <algorithm>
+
+#include "bessel.cuh"
+#include "fft_block.cuh"
+#include "plans.hpp"
+
+namespace nb {
+
+namespace {
+
+constexpr int kMaxSamplesPerThread = 18;
+
+struct Pass1Params {
+    long long n;      // N
+    int log_n1, log_n2;
+    int r0, r1;       // terms [r0, r1)
+};
+
+// ------------------------------------------------------------------ pass 1
+template <int L1, bool UNIFORM>
+__global__ void __launch_bounds__(L1 / 16)
+    k2_pass1(const double2* __restrict__ c, double2* __restrict__ Y, Pass1Params p,
+             const double2* __restrict__ tw) {
+    constexpr int G = L1 / 16;
+    extern __shared__ double2 smem[];
+    double2* cbuf = smem;                       // L1 (own-thread slots)
+    double2* buf0 = cbuf + L1;                  // padded
+    double2* buf1 = buf0 + padded_len(L1);      // padded
+    double2* step = buf1 + padded_len(L1);      // 16 twiddle steps
+    const int tid = threadIdx.x;
+    const long long n2 = 1ll << p.log_n2;
+    const long long N = p.n;
+    for (long long k2 = blockIdx.x; k2 < n2; k2 += gridDim.x) {
+        // column k2 of c: k = k1*N2 + k2, k1 = tid + q*G
+#pragma unroll
+        for (int q = 0; q < 16; ++q) cbuf[tid + q * G] = __ldg(c + (((long long)(tid + q * G)) << p.log_n2) + k2);
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2*q*G}
+        const double2 base = unit_root(k2 * tid, N);            // w_N^{k2*tid}
+        // 2*s_q = 4k/N - 2 = 4(tid*N2 + k2)/N - 2 + q/4   (exact)
+        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+        double tcur[16], tprev[16];
+        if constexpr (!UNIFORM) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                tprev[q] = 1.0;                         // T_0
+                tcur[q] = 0.5 * (two_s0 + 0.25 * q);    // T_1 = s
+            }
+            // advance to r0: (tprev, tcur) = (T_{r0-1}, T_{r0}) ; r0 == 0 keeps (., T_0)
+            for (int r = 1; r < p.r0; ++r) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                    tprev[q] = tcur[q];
+                    tcur[q] = tn;
+                }
+            }
+        }
+        __syncthreads();
+        for (int r = p.r0; r < p.r1; ++r) {
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 cv = cbuf[tid + q * G];
+                if constexpr (UNIFORM) {
+                    v[q] = cv;
+                } else {
+                    const double vr = (r == 0) ? 0.5 : (r == 1 ? tcur[q] : tcur[q]);
+                    v[q] = make_double2(cv.x * vr, cv.y * vr);
+                }
+            }
+            block_fft<L1, -1>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
+            double2* out = Y + (long long)(r - p.r0) * N + k2;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 w = cmul(base, step[q]);
+                const long long t1 = tid + q * G;
+                out[t1 << p.log_n2] = cmul(v[q], w);
+            }
+            if constexpr (!UNIFORM) {
+                // (tprev, tcur) <- (T_r, T_{r+1});  r == 0: T_1 = s already in tcur
+                if (r == 0) {
+                    // tcur holds T_1 from init when r0 == 0; nothing to advance
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                        tprev[q] = tcur[q];
+                        tcur[q] = tn;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// pass 1 for N1 == 1: Y_r[k] = v_r(k) c[k]
+__global__ void k2_scale(const double2* __restrict__ c, double2* __restrict__ Y, long long N,
+                         int r0, int r1, int uniform) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const double2 cv = c[k];
+    if (uniform) {
+        Y[k] = cv;
+        return;
+    }
+    const double s = __dsub_rn(__dmul_rn(2.0, (double)k / (double)N), 1.0);
+    double tprev = 1.0, tcur = s;
+    for (int r = 0; r < r1; ++r) {
+        double vr;
+        if (r == 0) {
+            vr = 0.5;
+        } else {
+            if (r >= 2) {
+                const double tn = __fma_rn(2.0 * s, tcur, -tprev);
+                tprev = tcur;
+                tcur = tn;
+            }
+            vr = tcur;
+        }
+        if (r >= r0) Y[(long long)(r - r0) * N + k] = make_double2(cv.x * vr, cv.y * vr);
+    }
+}
+
+// ------------------------------------------------------------------ pass 2
+struct Pass2Params {
+    long long n;
+    int log_n1, log_n2;
+    int r0, r1;
+    const double* xs;
+    const int* perm;
+    const int* rowoff;
+    int deg[kRankCap];
+};
+
+template <int D, int Q, int G>
+__device__ __forceinline__ void horner_update(double2 (&acc)[Q], int r, const double2* xb,
+                                              const int* st2, const double* sh, int tid, int cnt) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int i = tid + q * G;
+        if (i < cnt) {
+            const double h = sh[i];
+            const double2 X = xb[st2[i]];
+            const double g = bessel_g<D>(r, h * h);
+            const double ax = acc[q].x;
+            acc[q].x = __fma_rn(g, X.x, -h * acc[q].y);
+            acc[q].y = __fma_rn(g, X.y, h * ax);
+        }
+    }
+}
+
+template <int Q, int G>
+__device__ __forceinline__ void horner_dispatch(int deg, double2 (&acc)[Q], int r, const double2* xb,
+                                                const int* st2, const double* sh, int tid, int cnt) {
+    switch (deg) {
+#define NB_CASE(D) \
+    case D: horner_update<D, Q, G>(acc, r, xb, st2, sh, tid, cnt); break;
+        NB_CASE(0) NB_CASE(1) NB_CASE(2) NB_CASE(3) NB_CASE(4) NB_CASE(5) NB_CASE(6) NB_CASE(7)
+        NB_CASE(8) NB_CASE(9) NB_CASE(10) NB_CASE(11) NB_CASE(12) NB_CASE(13) NB_CASE(14)
+        default: horner_update<15, Q, G>(acc, r, xb, st2, sh, tid, cnt); break;
+#undef NB_CASE
+    }
+}
+
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(L2 / 16, 1)
+    k2_pass2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p,
+             const double2* __restrict__ tw) {
+    constexpr int G = L2 / 16;
+    constexpr int Q = kMaxSamplesPerThread;
+    constexpr int CAP = Q * G;
+    extern __shared__ double2 smem[];
+    double2* buf0 = smem;
+    double2* buf1 = buf0 + padded_len(L2);
+    double* sh = reinterpret_cast<double*>(buf1 + padded_len(L2));  // CAP
+    int* st2 = reinterpret_cast<int*>(sh + CAP);                    // CAP
+    const int tid = threadIdx.x;
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const long long n2 = 1ll << p.log_n2;
+    const double dn = (double)N;
+    double2* xb = block_fft_free_buf<L2>(buf0, buf1);
+    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        for (int cb = beg; cb < end; cb += CAP) {
+            const int cnt = min(CAP, end - cb);
+            double2 acc[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                acc[q] = make_double2(0.0, 0.0);
+                const int i = tid + q * G;
+                if (i < cnt) {
+                    const double x = p.xs[cb + i];
+                    const double pr = __dmul_rn(dn, x);
+                    const long long sj = (long long)round(pr);
+                    const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                    const long long t = sj & (N - 1);
+                    st2[i] = (int)(t >> p.log_n1);
+                    sh[i] = half_phase(d);
+                }
+            }
+            for (int r = p.r1 - 1; r >= p.r0; --r) {
+                const double2* row_in = Y + (long long)(r - p.r0) * N + (row << p.log_n2);
+                if (r > p.r0) {
+                    // warm L2 with the next row while this one is transformed
+                    if (tid == 0) {
+                        const void* nxt = Y + (long long)(r - 1 - p.r0) * N + (row << p.log_n2);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                                     "r"((unsigned)(n2 * sizeof(double2))) : "memory");
+                    }
+                }
+                double2 v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = row_in[tid + q * G];
+                block_fft<L2, -1>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
+#pragma unroll
+                for (int q = 0; q < 16; ++q) xb[tid + q * G] = v[q];
+                __syncthreads();
+                if constexpr (UNIFORM) {
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        const int i = tid + q * G;
+                        if (i < cnt) acc[q] = xb[st2[i]];
+                    }
+                } else {
+                    horner_dispatch<Q, G>(p.deg[r], acc, r, xb, st2, sh, tid, cnt);
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int i = tid + q * G;
+                if (i < cnt) {
+                    double2 out = acc[q];
+                    if constexpr (!UNIFORM) {
+                        const double h = sh[i];
+                        if (p.r0 > 0) {  // restore the (i h)^r0 factor of a partial term range
+                            double hr = 1.0;
+                            for (int k = 0; k < p.r0; ++k) hr *= h;
+                            out = cscale(out, hr);
+                            switch (p.r0 & 3) {
+                                case 1: out = make_double2(-out.y, out.x); break;
+                                case 2: out = make_double2(-out.x, -out.y); break;
+                                case 3: out = make_double2(out.y, -out.x); break;
+                                default: break;
+                            }
+                        }
+                        double sn, cs;
+                        sincos(2.0 * h, &sn, &cs);
+                        out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+                    }
+                    f[p.perm[cb + i]] = out;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launch
+template <int L>
+constexpr size_t pass1_smem() {
+    return sizeof(double2) * (L + 2 * padded_len(L) + 16);
+}
+template <int L>
+constexpr size_t pass2_smem() {
+    return sizeof(double2) * 2 * padded_len(L) + (sizeof(double) + sizeof(int)) * kMaxSamplesPerThread * (L / 16);
+}
+
+template <class F>
+void set_smem(F* fn, size_t bytes, int device) {
+    (void)device;
+    NB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+int occupancy(const void* fn, int threads, size_t smem) {
+    int n = 0;
+    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    return std::max(1, n);
+}
+
+template <int L1>
+void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int r1,
+                  cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    constexpr size_t SM = pass1_smem<L1>();
+    Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+    const long long n2 = 1ll << pl.bk.log_n2;
+    if (pl.uniform) {
+        auto fn = k2_pass1<L1, true>;
+        set_smem(fn, SM, pl.device);
+        const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
+        fn<<<grid, L1 / 16, SM, s>>>(c, Y, p, ctx.table(L1));
+    } else {
+        auto fn = k2_pass1<L1, false>;
+        set_smem(fn, SM, pl.device);
+        const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
+        fn<<<grid, L1 / 16, SM, s>>>(c, Y, p, ctx.table(L1));
+    }
+    NB_LAUNCH();
+}
+
+template <int L2>
+void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int r1,
+                  cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    constexpr size_t SM = pass2_smem<L2>();
+    Pass2Params p{};
+    p.n = (long long)pl.n;
+    p.log_n1 = pl.bk.log_n1;
+    p.log_n2 = pl.bk.log_n2;
+    p.r0 = r0;
+    p.r1 = r1;
+    p.xs = pl.bk.xs.as<double>();
+    p.perm = pl.bk.perm.as<int>();
+    p.rowoff = pl.bk.rowoff.as<int>();
+    for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
+    const long long n1 = 1ll << pl.bk.log_n1;
+    if (pl.uniform) {
+        auto fn = k2_pass2<L2, true>;
+        set_smem(fn, SM, pl.device);
+        const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, L2 / 16, SM));
+        fn<<<grid, L2 / 16, SM, s>>>(Y, f, p, ctx.table(L2));
+    } else {
+        auto fn = k2_pass2<L2, false>;
+        set_smem(fn, SM, pl.device);
+        const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, L2 / 16, SM));
+        fn<<<grid, L2 / 16, SM, s>>>(Y, f, p, ctx.table(L2));
+    }
+    NB_LAUNCH();
+}
+
+void dispatch_pass1(int L, const double2* c, double2* Y, const CorePlan& pl, int r0, int r1,
+                    cudaStream_t s) {
+    switch (L) {
+        case 16: return launch_pass1<16>(c, Y, pl, r0, r1, s);
+        case 32: return launch_pass1<32>(c, Y, pl, r0, r1, s);
+        case 64: return launch_pass1<64>(c, Y, pl, r0, r1, s);
+        case 128: return launch_pass1<128>(c, Y, pl, r0, r1, s);
+        case 256: return launch_pass1<256>(c, Y, pl, r0, r1, s);
+        case 512: return launch_pass1<512>(c, Y, pl, r0, r1, s);
+        case 1024: return launch_pass1<1024>(c, Y, pl, r0, r1, s);
+        case 2048: return launch_pass1<2048>(c, Y, pl, r0, r1, s);
+        case 4096: return launch_pass1<4096>(c, Y, pl, r0, r1, s);
+        default: throw Error(kInternal, "pass1 size");
+    }
+}
+void dispatch_pass2(int L, const double2* Y, double2* f, const CorePlan& pl, int r0, int r1,
+                    cudaStream_t s) {
+    switch (L) {
+        case 16: return launch_pass2<16>(Y, f, pl, r0, r1, s);
+        case 32: return launch_pass2<32>(Y, f, pl, r0, r1, s);
+        case 64: return launch_pass2<64>(Y, f, pl, r0, r1, s);
+        case 128: return launch_pass2<128>(Y, f, pl, r0, r1, s);
+        case 256: return launch_pass2<256>(Y, f, pl, r0, r1, s);
+        case 512: return launch_pass2<512>(Y, f, pl, r0, r1, s);
+        case 1024: return launch_pass2<1024>(Y, f, pl, r0, r1, s);
+        case 2048: return launch_pass2<2048>(Y, f, pl, r0, r1, s);
+        case 4096: return launch_pass2<4096>(Y, f, pl, r0, r1, s);
+        default: throw Error(kInternal, "pass2 size");
+    }
+}
+
+// ------------------------------------------------------------------ generic
+__global__ void k2g_scale(const double2* __restrict__ c, double2* __restrict__ w, long long n,
+                          int r) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double vr = v_factor_from_s(grid_s(k, n), r);
+    const double2 cv = c[k];
+    w[k] = make_double2(cv.x * vr, cv.y * vr);
+}
+
+__global__ void k2g_accum(const double2* __restrict__ X, double2* __restrict__ f,
+                          const double* __restrict__ delta, const long long* __restrict__ t,
+                          long long n, int r, int deg, int first, int uniform) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double2 x = X[t[j]];
+    double2 term;
+    if (uniform) {
+        term = x;
+    } else {
+        term = cmul(u_factor(delta[j], r, deg), x);
+    }
+    f[j] = first ? term : cadd(f[j], term);
+}
+
+inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void exec_type2(const CorePlan& pl, const double2* c, double2* f, size_t batch, size_t r0,
+                size_t r1, cudaStream_t s, cudaEvent_t* ev) {
+    ensure_bessel_constants(pl.device);
+    const size_t N = pl.n;
+    if (r1 > pl.K) r1 = pl.K;
+    if (r0 >= r1) {
+        NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * N * batch, s));
+        return;
+    }
+    if (pl.fused) {
+        const size_t nt = r1 - r0;
+        DevBuf Y(sizeof(double2) * N * nt, s);
+        const int L1 = 1 << pl.bk.log_n1, L2 = 1 << pl.bk.log_n2;
+        for (size_t b = 0; b < batch; ++b) {
+            const double2* cb = c + b * N;
+            double2* fb = f + b * N;
+            if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[0], s));
+            if (pl.bk.log_n1 == 0) {
+                k2_scale<<<blocks(N), 256, 0, s>>>(cb, Y.as<double2>(), (long long)N, (int)r0,
+                                                   (int)r1, pl.uniform ? 1 : 0);
+                NB_LAUNCH();
+            } else {
+                dispatch_pass1(L1, cb, Y.as<double2>(), pl, (int)r0, (int)r1, s);
+            }
+            if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[1], s));
+            dispatch_pass2(L2, Y.as<double2>(), fb, pl, (int)r0, (int)r1, s);
+            if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[2], s));
+        }
+        return;
+    }
+    // generic path: per-term scale -> FFT -> gather/accumulate (ascending r)
+    DevBuf w(sizeof(double2) * N, s);
+    for (size_t b = 0; b < batch; ++b) {
+        const double2* cb = c + b * N;
+        double2* fb = f + b * N;
+        for (size_t r = r0; r < r1; ++r) {
+            if (pl.uniform) {
+                NB_CUDA(cudaMemcpyAsync(w.get(), cb, sizeof(double2) * N, cudaMemcpyDeviceToDevice, s));
+            } else {
+                k2g_scale<<<blocks(N), 256, 0, s>>>(cb, w.as<double2>(), (long long)N, (int)r);
+                NB_LAUNCH();
+            }
+            fft_exec(w.as<double2>(), w.as<double2>(), N, 1, -1, s, pl.device);
+            k2g_accum<<<blocks(N), 256, 0, s>>>(w.as<double2>(), fb, pl.ax.delta.as<double>(),
+                                                pl.ax.t.as<long long>(), (long long)N, (int)r,
+                                                pl.series_deg.empty() ? 15 : pl.series_deg[r],
+                                                r == r0 ? 1 : 0, pl.uniform ? 1 : 0);
+            NB_LAUNCH();
+        }
+    }
+}
+
+}  // namespace nb
