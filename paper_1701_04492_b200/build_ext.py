@@ -65,7 +65,24 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr)
         os.replace(tmp, LIB)
+    _build_example()
     return LIB
+
+
+EXAMPLE_SRC = os.path.join(HERE, "..", "tests", "cpp", "example_dropin.cpp")
+EXAMPLE_BIN = os.path.join(OBJ, "example_dropin")
+
+
+def _build_example() -> None:
+    """The C++ drop-in usage example (include/nufft headers + libnufft_b200.so)."""
+    if os.path.exists(EXAMPLE_BIN) and os.path.getmtime(EXAMPLE_BIN) >= max(
+            os.path.getmtime(LIB), os.path.getmtime(EXAMPLE_SRC)):
+        return
+    r = subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(HERE, "..", "include"),
+                        EXAMPLE_SRC, "-o", EXAMPLE_BIN, "-L" + HERE, "-lnufft_b200",
+                        "-Wl,-rpath,$ORIGIN/.."], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("example build failed:\n" + r.stderr)
 
 
 if __name__ == "__main__":
