@@ -18,9 +18,16 @@ namespace {
 
 inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
-// |delta| >= 0, so the IEEE bit pattern orders like the value
+// |delta| >= 0, so the IEEE bit pattern orders like the value.  Reduced over
+// the warp first (one atomic per warp instead of one per sample: a single
+// contended address otherwise serializes 2^24 atomics).
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* dst, double v) {
-    atomicMax(dst, (unsigned long long)__double_as_longlong(v));
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, b, o);
+        b = other > b ? other : b;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(dst, b);
 }
 
 // transforms.hpp:35-45 + :77-92 (+ :60-64 exact delta)
@@ -29,24 +36,27 @@ __global__ void k_assign_samples(const double* __restrict__ raw, long long n, lo
                                  long long* __restrict__ t, double* __restrict__ delta,
                                  unsigned long long* gamma_bits, int* bad) {
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const double r = raw[j];
-    if (!isfinite(r)) {
-        atomicOr(bad, 1);
-        return;
+    double gam = 0.0;
+    if (j < n) {
+        const double r = raw[j];
+        if (!isfinite(r)) {
+            atomicOr(bad, 1);
+        } else {
+            double v = __dsub_rn(r, floor(r));
+            if (v >= 1.0) v = 0.0;
+            const double dn = (double)grid;
+            const double p = __dmul_rn(dn, v);
+            const long long sj = (long long)round(p);
+            const double err = __fma_rn(dn, v, -p);
+            const double d = __dadd_rn(__dsub_rn(p, (double)sj), err);
+            x[j] = v;
+            s[j] = sj;
+            t[j] = sj % grid;
+            delta[j] = d;
+            gam = fabs(d);
+        }
     }
-    double v = __dsub_rn(r, floor(r));
-    if (v >= 1.0) v = 0.0;
-    const double dn = (double)grid;
-    const double p = __dmul_rn(dn, v);
-    const long long sj = (long long)round(p);
-    const double err = __fma_rn(dn, v, -p);
-    const double d = __dadd_rn(__dsub_rn(p, (double)sj), err);
-    x[j] = v;
-    s[j] = sj;
-    t[j] = sj % grid;
-    delta[j] = d;
-    atomic_max_nonneg(gamma_bits, fabs(d));
+    atomic_max_nonneg(gamma_bits, gam);
 }
 
 // transforms.hpp:246-277: omega in [0, N] (type I) or [0, N) (type III, upper_open)
@@ -55,23 +65,26 @@ __global__ void k_assign_freqs(const double* __restrict__ omega, long long n, in
                                long long* __restrict__ t, double* __restrict__ delta,
                                unsigned long long* gamma_bits, int* bad) {
     const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const double w = omega[k];
-    const double dn = (double)n;
-    if (!isfinite(w) || w < 0.0 || w > dn || (upper_open && !(w < dn))) {
-        atomicOr(bad, 1);
-        return;
+    double gam = 0.0;
+    if (k < n) {
+        const double w = omega[k];
+        const double dn = (double)n;
+        if (!isfinite(w) || w < 0.0 || w > dn || (upper_open && !(w < dn))) {
+            atomicOr(bad, 1);
+        } else {
+            const double scaled = __ddiv_rn(w, dn);
+            double v = __dsub_rn(scaled, floor(scaled));
+            if (v >= 1.0) v = 0.0;
+            const long long sk = (long long)round(w);
+            const double d = __dsub_rn(w, (double)sk);
+            x[k] = v;
+            s[k] = sk;
+            t[k] = sk % n;
+            delta[k] = d;
+            gam = fabs(d);
+        }
     }
-    const double scaled = __ddiv_rn(w, dn);
-    double v = __dsub_rn(scaled, floor(scaled));
-    if (v >= 1.0) v = 0.0;
-    const long long sk = (long long)round(w);
-    const double d = __dsub_rn(w, (double)sk);
-    x[k] = v;
-    s[k] = sk;
-    t[k] = sk % n;
-    delta[k] = d;
-    atomic_max_nonneg(gamma_bits, fabs(d));
+    atomic_max_nonneg(gamma_bits, gam);
 }
 
 __global__ void k_bucket_keys(const long long* __restrict__ t, long long n, int log_n1, int log_n2,
