@@ -133,11 +133,94 @@ struct FftShape {
     static_assert(L >= 16 && L <= 4096 && (1 << LOG) == L, "block FFT size");
 };
 
-// Twiddle exp(SIGN*2*pi*i*m/L) from the forward table tw (tw[m] = exp(-2*pi*i*m/L)).
+// ---------------------------------------------------------------- twiddles
+// Stage twiddles without table gathers (a scattered 16-byte L1 gather per
+// twiddle cost more than the whole DFT arithmetic in microbenchmarks):
+//  * the Ns = 16 stage uses w_{16 R2}^{k t}, k = j mod 16: a 16 x R2 table in
+//    shared memory laid out [t][k] (one warp load touches 16 consecutive
+//    entries: 2 wavefronts, no conflicts);
+//  * the Ns = 256 stage (L >= 512) uses w_L^{k t} with k = j < 256, i.e. a
+//    per-thread set: bases w^k, w^{2k}, w^{4k}, w^{8k} are evaluated once per
+//    kernel (sincospi, correctly rounded argument) and the other powers are
+//    products of at most three of them (<= ~3 ulp).
+template <int L>
+struct FftShapeX : FftShape<L> {
+    static constexpr int R_LAST = (FftShape<L>::REM > 1) ? FftShape<L>::REM : 16;
+    static constexpr int R2 = (FftShape<L>::STAGES == 2) ? R_LAST : 16;  // radix of the Ns=16 stage
+    static constexpr int R3 = (FftShape<L>::STAGES == 3) ? R_LAST : 1;   // radix of the Ns=256 stage
+    static constexpr int B3 = 16 / R3;                                    // its butterflies per thread
+    static constexpr int T16_LEN = (FftShape<L>::STAGES >= 2) ? 16 * R2 : 16;
+};
+
+template <int L>
+struct Twiddles {
+    using X = FftShapeX<L>;
+    const double2* t16;                       // shared: t16[t*16 + k] = w_{16 R2}^{k t} (forward)
+    double2 b[X::STAGES == 3 ? X::B3 : 1][4];  // stage-3 bases per butterfly: w^k, w^2k, w^4k, w^8k
+};
+
+// fill the Ns=16 table (all threads of the CTA; barrier before use)
+template <int L>
+__device__ __forceinline__ void twiddle_table_build(double2* t16, int tid, int nthreads) {
+    using X = FftShapeX<L>;
+    for (int i = tid; i < X::T16_LEN; i += nthreads) {
+        const int t = i >> 4, k = i & 15;
+        t16[i] = unit_root((long long)k * t, 16 * X::R2);
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void twiddle_init(Twiddles<L>& T, const double2* t16, int tid) {
+    using X = FftShapeX<L>;
+    T.t16 = t16;
+    if constexpr (X::STAGES == 3) {
+#pragma unroll
+        for (int bb = 0; bb < X::B3; ++bb) {
+            const long long k = tid + bb * (L / 16);  // j < 256: k = j
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                T.b[bb][e] = (X::R3 > (1 << e)) ? unit_root((k << e) % L, L) : make_double2(1.0, 0.0);
+        }
+    }
+}
+
 template <int SIGN>
-__device__ __forceinline__ double2 tw_fetch(const double2* __restrict__ tw, int m) {
-    const double2 w = __ldg(tw + m);
+__device__ __forceinline__ double2 tw_sign(double2 w) {
     return SIGN < 0 ? w : make_double2(w.x, -w.y);
+}
+
+// a[t] *= w^t (t = 1..R-1) for the Ns = 256 stage, powers from the bases
+template <int R, int SIGN>
+__device__ __forceinline__ void apply_pow_twiddles(double2* a, const double2 (&bs)[4]) {
+    const double2 p1 = tw_sign<SIGN>(bs[0]);
+    if constexpr (R == 2) {
+        a[1] = cmul(a[1], p1);
+    } else {
+        const double2 p2 = tw_sign<SIGN>(bs[1]);
+        const double2 p3 = cmul(p1, p2);
+        a[1] = cmul(a[1], p1);
+        a[2] = cmul(a[2], p2);
+        a[3] = cmul(a[3], p3);
+        if constexpr (R >= 8) {
+            const double2 p4 = tw_sign<SIGN>(bs[2]);
+            const double2 p5 = cmul(p1, p4), p6 = cmul(p2, p4), p7 = cmul(p3, p4);
+            a[4] = cmul(a[4], p4);
+            a[5] = cmul(a[5], p5);
+            a[6] = cmul(a[6], p6);
+            a[7] = cmul(a[7], p7);
+            if constexpr (R == 16) {
+                const double2 p8 = tw_sign<SIGN>(bs[3]);
+                a[8] = cmul(a[8], p8);
+                a[9] = cmul(a[9], cmul(p1, p8));
+                a[10] = cmul(a[10], cmul(p2, p8));
+                a[11] = cmul(a[11], cmul(p3, p8));
+                a[12] = cmul(a[12], cmul(p4, p8));
+                a[13] = cmul(a[13], cmul(p5, p8));
+                a[14] = cmul(a[14], cmul(p6, p8));
+                a[15] = cmul(a[15], cmul(p7, p8));
+            }
+        }
+    }
 }
 
 // One Stockham stage: radix R, Ns = product of the radices already applied.
@@ -145,7 +228,7 @@ __device__ __forceinline__ double2 tw_fetch(const double2* __restrict__ tw, int 
 // (padded, natural Stockham order); if LAST leaves it in v (same layout).
 template <int L, int R, int NS, bool LAST, int SIGN>
 __device__ __forceinline__ void stockham_stage(double2 (&v)[16], double2* out, int tid,
-                                               const double2* __restrict__ tw) {
+                                               const Twiddles<L>& T) {
     constexpr int G = L / 16;
     constexpr int B = 16 / R;  // butterflies per thread
 #pragma unroll
@@ -155,10 +238,13 @@ __device__ __forceinline__ void stockham_stage(double2 (&v)[16], double2* out, i
         double2 a[R];
 #pragma unroll
         for (int t = 0; t < R; ++t) a[t] = v[b + t * B];
-        if constexpr (NS > 1) {
-            constexpr int STEP = L / (NS * R);
+        if constexpr (NS == 16) {
 #pragma unroll
-            for (int t = 1; t < R; ++t) a[t] = cmul(a[t], tw_fetch<SIGN>(tw, k * t * STEP));
+            for (int t = 1; t < R; ++t) a[t] = cmul(a[t], tw_sign<SIGN>(T.t16[t * 16 + k]));
+        } else if constexpr (NS == 256) {
+            apply_pow_twiddles<R, SIGN>(a, T.b[b]);
+        } else {
+            static_assert(NS == 1, "stage");
         }
         dft<R, SIGN>(a);
         if constexpr (LAST) {
@@ -181,30 +267,56 @@ __device__ __forceinline__ void load_stage_input(double2 (&v)[16], const double2
 
 // Full L-point FFT on the register array v (layout above).  buf0/buf1: two
 // padded shared buffers of padded_len(L) double2 owned by this group; `bar`
-// is the group barrier.  tw: forward table exp(-2*pi*i*m/L), m < L.
-// On exit the last-written buffer is buf[(STAGES-2)&1]; the other one is free.
+// is the group barrier.  On exit the last-written buffer is
+// buf[(STAGES-2)&1]; the other one is free.
 template <int L, int SIGN, class Bar>
 __device__ __forceinline__ void block_fft(double2 (&v)[16], double2* buf0, double2* buf1, int tid,
-                                          const double2* __restrict__ tw, Bar bar) {
-    using S = FftShape<L>;
-    constexpr int R_LAST = (S::REM > 1) ? S::REM : 16;
+                                          const Twiddles<L>& T, Bar bar) {
+    using S = FftShapeX<L>;
     if constexpr (S::STAGES == 1) {
-        stockham_stage<L, 16, 1, true, SIGN>(v, nullptr, tid, tw);
+        stockham_stage<L, 16, 1, true, SIGN>(v, nullptr, tid, T);
     } else if constexpr (S::STAGES == 2) {
-        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, tw);
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, T);
         bar();
         load_stage_input<L>(v, buf0, tid);
-        stockham_stage<L, R_LAST, 16, true, SIGN>(v, nullptr, tid, tw);
-    } else if constexpr (S::STAGES == 3) {
-        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, tw);
+        stockham_stage<L, S::R_LAST, 16, true, SIGN>(v, nullptr, tid, T);
+    } else {
+        static_assert(S::STAGES == 3, "L <= 4096");
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf0, tid, T);
         bar();
         load_stage_input<L>(v, buf0, tid);
-        stockham_stage<L, 16, 16, false, SIGN>(v, buf1, tid, tw);
+        stockham_stage<L, 16, 16, false, SIGN>(v, buf1, tid, T);
         bar();
         load_stage_input<L>(v, buf1, tid);
-        stockham_stage<L, R_LAST, 256, true, SIGN>(v, nullptr, tid, tw);
+        stockham_stage<L, S::R_LAST, 256, true, SIGN>(v, nullptr, tid, T);
+    }
+}
+
+// Single-buffer variant (half the shared memory of block_fft): each exchange
+// is write -> barrier -> read -> barrier.  The caller guarantees `buf` is free
+// on entry; on exit other threads may still be reading it for the final stage,
+// so the caller must barrier before writing `buf` again.
+template <int L, int SIGN, class Bar>
+__device__ __forceinline__ void block_fft_1buf(double2 (&v)[16], double2* buf, int tid,
+                                               const Twiddles<L>& T, Bar bar) {
+    using S = FftShapeX<L>;
+    if constexpr (S::STAGES == 1) {
+        stockham_stage<L, 16, 1, true, SIGN>(v, nullptr, tid, T);
+    } else if constexpr (S::STAGES == 2) {
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf, tid, T);
+        bar();
+        load_stage_input<L>(v, buf, tid);
+        stockham_stage<L, S::R_LAST, 16, true, SIGN>(v, nullptr, tid, T);
     } else {
-        static_assert(S::STAGES <= 3, "L <= 4096");
+        static_assert(S::STAGES == 3, "L <= 4096");
+        stockham_stage<L, 16, 1, false, SIGN>(v, buf, tid, T);
+        bar();
+        load_stage_input<L>(v, buf, tid);
+        bar();
+        stockham_stage<L, 16, 16, false, SIGN>(v, buf, tid, T);
+        bar();
+        load_stage_input<L>(v, buf, tid);
+        stockham_stage<L, S::R_LAST, 256, true, SIGN>(v, nullptr, tid, T);
     }
 }
 

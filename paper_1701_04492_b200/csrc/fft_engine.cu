@@ -31,13 +31,18 @@ __global__ void __launch_bounds__(kBlockThreads) k_fft_block(const double2* in, 
     const int tid = threadIdx.x % G;
     double2* buf0 = smem + g * 2 * padded_len(L);
     double2* buf1 = buf0 + padded_len(L);
+    double2* t16 = smem + GPC * 2 * padded_len(L);
+    twiddle_table_build<L>(t16, threadIdx.x, blockDim.x);
+    Twiddles<L> T;
+    twiddle_init<L>(T, t16, tid);
     const size_t b = static_cast<size_t>(blockIdx.x) * GPC + g;
     const bool live = b < batch;
     double2 v[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q)
         v[q] = live ? in[b * L + tid + q * G] : make_double2(0.0, 0.0);
-    block_fft<L, SIGN>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
+    __syncthreads();
+    block_fft<L, SIGN>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
     if (live) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) out[b * L + tid + q * G] = v[q];
@@ -50,7 +55,7 @@ constexpr int block_groups() {
 }
 template <int L>
 constexpr size_t block_smem() {
-    return sizeof(double2) * 2 * padded_len(L) * block_groups<L>();
+    return sizeof(double2) * (2 * padded_len(L) * block_groups<L>() + FftShapeX<L>::T16_LEN);
 }
 
 template <int L, int SIGN>
@@ -100,6 +105,10 @@ __global__ void __launch_bounds__(kBlockThreads)
     const int tid = threadIdx.x % G;
     double2* buf0 = smem + g * 2 * padded_len(L);
     double2* buf1 = buf0 + padded_len(L);
+    double2* t16 = smem + GPC * 2 * padded_len(L);
+    twiddle_table_build<L>(t16, threadIdx.x, blockDim.x);
+    Twiddles<L> T;
+    twiddle_init<L>(T, t16, tid);
     const long long j = static_cast<long long>(blockIdx.x) * GPC + g;
     const bool live = j < nbutterfly;
     const size_t boff = static_cast<size_t>(blockIdx.y) * n;
@@ -117,7 +126,8 @@ __global__ void __launch_bounds__(kBlockThreads)
         }
         v[q] = x;
     }
-    block_fft<L, SIGN>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
+    __syncthreads();
+    block_fft<L, SIGN>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
     if (live) {
         const long long base = (j - k) * L + k;
 #pragma unroll

@@ -6,22 +6,24 @@
 // (accumulate_term :152-161).  Here the K terms are fused into two passes of
 // a four-step FFT, N = N1 * N2 (k = k1*N2 + k2, t = t1 + N1*t2):
 //
-//  pass 1 (one CTA per column k2, persistent): the c column (N1 values) is
-//    read ONCE from HBM; for every r the v_r scaling (Chebyshev recurrence in
-//    registers) is applied on the fly, the N1-point column FFT runs in
-//    registers/shared memory, the inter-pass twiddle w_N^{t1 k2} is applied
-//    and Y_r[t1][k2] is written (the only HBM round trip of the K spectra).
-//  pass 2 (one CTA per row t1, persistent): for r = K-1 .. 0 the row Y_r[t1][:]
-//    is read, its N2-point FFT gives X_r[t1 + N1 t2] in shared memory, and every
-//    sample bucketed on this row (t_j mod N1 == t1, plan-time sort) gathers
-//    X_r[t2_j] into a per-sample register accumulator by Horner in r:
-//        acc <- acc * (i h_j) + g_r(h_j^2) X_r[t2_j]
+//  pass 1 (CTA per column k2, persistent, two CTAs per SM): for every r the
+//    column c[k1*N2 + k2] is read (from HBM once, then L2), scaled by
+//    v_r = T_r(2k/N - 1) (Chebyshev recurrence evaluated in registers), the
+//    N1-point column FFT runs in registers + one shared exchange buffer, the
+//    inter-pass twiddle w_N^{t1 k2} is applied and Y_r[t1][k2] is written
+//    (the only HBM round trip of the K spectra).
+//  pass 2 (CTA per row t1, persistent, warp-specialized): FFT warps transform
+//    Y_r[t1][:] for r = K-1 .. 0 into X_r[t1 + N1 t2] (double-buffered shared
+//    memory); sample warps, overlapped one r behind, gather X_r[t2_j] for every
+//    sample bucketed on this row (t_j mod N1 == t1, plan-time sort) into a
+//    per-sample register accumulator by Horner in r,
+//        acc <- acc * (i h_j) + g_r(h_j^2) X_r[t2_j],
 //    which sums u_r[j] X_r[t_j] over r without materializing u (Bessel form,
-//    bessel.cuh).  The scaled result 2 exp(2 i h_j) acc is written once to f[j].
+//    bessel.cuh).  2 exp(2 i h_j) acc is written once to f[j].
 //
 // HBM bytes per point (batch 1): c 16 + f 16 + xs/perm 12 + 32 K (Y written
 // and read once) — SURVEY.md §8(d).  No atomics: every f[j] is owned by one
-// thread, and sums run in a fixed order, so results are bit-reproducible.
+// thread and sums run in a fixed order, so results are bit-reproducible.
 #include <algorithm>
 
 #include "bessel.cuh"
@@ -34,43 +36,70 @@ namespace {
 
 constexpr int kMaxSamplesPerThread = 18;
 
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Y layout (N1 >= 2): term rr of spectrum element (t1, k2) lives at
+//   rr*N + 2*((t1 >> 1)*N2 + k2) + (t1 & 1)
+// i.e. rows t1 and t1^1 are interleaved element by element.  In pass 1,
+// adjacent lanes hold adjacent t1 of one column, so every warp store writes
+// complete 32-byte sectors (16-byte column stores otherwise reach DRAM as
+// partial sectors that need a read-modify-write whenever the CTAs writing
+// the neighbouring columns drift apart).  Pass 2 reads a row at 32-byte
+// stride; the other half of each sector is the neighbouring row, transformed
+// concurrently by the adjacent CTA, and is served from L2.  N1 == 1 keeps
+// the natural layout rr*N + k2.
+__host__ __device__ __forceinline__ long long y_index(int rr, long long N, int log_n2, long long t1,
+                                                      long long k2) {
+    return rr * N + 2 * (((t1 >> 1) << log_n2) + k2) + (t1 & 1);
+}
+
 struct Pass1Params {
-    long long n;      // N
+    long long n;  // N
     int log_n1, log_n2;
-    int r0, r1;       // terms [r0, r1)
+    int r0, r1;  // terms [r0, r1)
 };
 
 // ------------------------------------------------------------------ pass 1
+// The c column (N1 values, 16 B each) is read from HBM once per column into
+// shared memory (each thread only reads back its own slots); the Chebyshev
+// state (T_{r-1}, T_r) of the thread's 16 points lives in registers.
 template <int L1, bool UNIFORM>
-__global__ void __launch_bounds__(L1 / 16)
-    k2_pass1(const double2* __restrict__ c, double2* __restrict__ Y, Pass1Params p,
-             const double2* __restrict__ tw) {
+__global__ void __launch_bounds__(L1 / 16, 1)
+    k2_pass1(const double2* __restrict__ c, double2* __restrict__ Y, Pass1Params p) {
     constexpr int G = L1 / 16;
     extern __shared__ double2 smem[];
-    double2* cbuf = smem;                       // L1 (own-thread slots)
-    double2* buf0 = cbuf + L1;                  // padded
-    double2* buf1 = buf0 + padded_len(L1);      // padded
-    double2* step = buf1 + padded_len(L1);      // 16 twiddle steps
+    double2* cbuf = smem;                   // L1, own-thread slots
+    double2* buf0 = cbuf + L1;              // padded exchange buffers
+    double2* buf1 = buf0 + padded_len(L1);
+    double2* step = buf1 + padded_len(L1);  // 16 inter-pass twiddle steps
+    double2* t16 = step + 16;               // Ns=16 stage twiddles
     const int tid = threadIdx.x;
+    twiddle_table_build<L1>(t16, tid, G);
+    Twiddles<L1> T;
+    twiddle_init<L1>(T, t16, tid);
     const long long n2 = 1ll << p.log_n2;
     const long long N = p.n;
     for (long long k2 = blockIdx.x; k2 < n2; k2 += gridDim.x) {
-        // column k2 of c: k = k1*N2 + k2, k1 = tid + q*G
+        __syncthreads();  // previous column's readers of step are done
 #pragma unroll
         for (int q = 0; q < 16; ++q) cbuf[tid + q * G] = __ldg(c + (((long long)(tid + q * G)) << p.log_n2) + k2);
-        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2*q*G}
-        const double2 base = unit_root(k2 * tid, N);            // w_N^{k2*tid}
-        // 2*s_q = 4k/N - 2 = 4(tid*N2 + k2)/N - 2 + q/4   (exact)
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
+        const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
+        // 2 s_q = 4k/N - 2 with k = (tid + q G) N2 + k2  ->  two_s0 + q/4   (exact)
         const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
         double tcur[16], tprev[16];
         if constexpr (!UNIFORM) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-                tprev[q] = 1.0;                         // T_0
-                tcur[q] = 0.5 * (two_s0 + 0.25 * q);    // T_1 = s
+                tprev[q] = 1.0;                       // T_0
+                tcur[q] = 0.5 * (two_s0 + 0.25 * q);  // T_1 = s
             }
-            // advance to r0: (tprev, tcur) = (T_{r0-1}, T_{r0}) ; r0 == 0 keeps (., T_0)
-            for (int r = 1; r < p.r0; ++r) {
+            for (int r = 1; r < p.r0; ++r) {  // state for r0: (T_{r0-1}, T_{r0})
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
@@ -81,6 +110,7 @@ __global__ void __launch_bounds__(L1 / 16)
         }
         __syncthreads();
         for (int r = p.r0; r < p.r1; ++r) {
+            if constexpr (FftShape<L1>::STAGES < 3) __syncthreads();  // buf0 reuse across r
             double2 v[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -88,23 +118,19 @@ __global__ void __launch_bounds__(L1 / 16)
                 if constexpr (UNIFORM) {
                     v[q] = cv;
                 } else {
-                    const double vr = (r == 0) ? 0.5 : (r == 1 ? tcur[q] : tcur[q]);
+                    const double vr = (r == 0) ? 0.5 : tcur[q];
                     v[q] = make_double2(cv.x * vr, cv.y * vr);
                 }
             }
-            block_fft<L1, -1>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
-            double2* out = Y + (long long)(r - p.r0) * N + k2;
+            block_fft<L1, -1>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const double2 w = cmul(base, step[q]);
                 const long long t1 = tid + q * G;
-                out[t1 << p.log_n2] = cmul(v[q], w);
+                Y[y_index(r - p.r0, N, p.log_n2, t1, k2)] = cmul(v[q], w);
             }
             if constexpr (!UNIFORM) {
-                // (tprev, tcur) <- (T_r, T_{r+1});  r == 0: T_1 = s already in tcur
-                if (r == 0) {
-                    // tcur holds T_1 from init when r0 == 0; nothing to advance
-                } else {
+                if (r > 0) {  // (tprev, tcur) <- (T_r, T_{r+1}); after r == 0 the state already is (T_0, T_1)
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
@@ -114,7 +140,6 @@ __global__ void __launch_bounds__(L1 / 16)
                 }
             }
         }
-        __syncthreads();
     }
 }
 
@@ -187,57 +212,93 @@ __device__ __forceinline__ void horner_dispatch(int deg, double2 (&acc)[Q], int 
     }
 }
 
+// sample setup: recompute s, t, delta exactly (transforms.hpp:60-64,84-86) from sorted x
+template <int Q, int G>
+__device__ __forceinline__ void load_samples(const Pass2Params& p, int cb, int cnt, int tid,
+                                             int* st2, double* sh, double2 (&acc)[Q]) {
+    const double dn = (double)p.n;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        acc[q] = make_double2(0.0, 0.0);
+        const int i = tid + q * G;
+        if (i < cnt) {
+            const double x = p.xs[cb + i];
+            const double pr = __dmul_rn(dn, x);
+            const long long sj = (long long)round(pr);
+            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+            const long long t = sj & (p.n - 1);
+            st2[i] = (int)(t >> p.log_n1);
+            sh[i] = half_phase(d);
+        }
+    }
+}
+
+template <int Q, int G, bool UNIFORM>
+__device__ __forceinline__ void store_samples(const Pass2Params& p, int cb, int cnt, int tid,
+                                              const double* sh, double2 (&acc)[Q],
+                                              double2* __restrict__ f) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int i = tid + q * G;
+        if (i < cnt) {
+            double2 out = acc[q];
+            if constexpr (!UNIFORM) {
+                const double h = sh[i];
+                if (p.r0 > 0) {  // restore the (i h)^r0 factor of a partial term range
+                    double hr = 1.0;
+                    for (int k = 0; k < p.r0; ++k) hr *= h;
+                    out = cscale(out, hr);
+                    switch (p.r0 & 3) {
+                        case 1: out = make_double2(-out.y, out.x); break;
+                        case 2: out = make_double2(-out.x, -out.y); break;
+                        case 3: out = make_double2(out.y, -out.x); break;
+                        default: break;
+                    }
+                }
+                double sn, cs;
+                sincos(2.0 * h, &sn, &cs);
+                out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+            }
+            __stcs(f + p.perm[cb + i], out);
+        }
+    }
+}
+
+// Small rows (L2 < 1024): one group does both the FFT and the samples.
 template <int L2, bool UNIFORM>
-__global__ void __launch_bounds__(L2 / 16, 1)
-    k2_pass2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p,
-             const double2* __restrict__ tw) {
+__global__ void __launch_bounds__(L2 / 16)
+    k2_pass2_small(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
     constexpr int G = L2 / 16;
     constexpr int Q = kMaxSamplesPerThread;
     constexpr int CAP = Q * G;
     extern __shared__ double2 smem[];
     double2* buf0 = smem;
     double2* buf1 = buf0 + padded_len(L2);
-    double* sh = reinterpret_cast<double*>(buf1 + padded_len(L2));  // CAP
-    int* st2 = reinterpret_cast<int*>(sh + CAP);                    // CAP
+    double2* t16 = buf1 + padded_len(L2);
+    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::T16_LEN);
+    int* st2 = reinterpret_cast<int*>(sh + CAP);
     const int tid = threadIdx.x;
+    twiddle_table_build<L2>(t16, tid, G);
+    Twiddles<L2> T;
+    twiddle_init<L2>(T, t16, tid);
+    __syncthreads();
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
-    const long long n2 = 1ll << p.log_n2;
-    const double dn = (double)N;
     double2* xb = block_fft_free_buf<L2>(buf0, buf1);
     for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         for (int cb = beg; cb < end; cb += CAP) {
             const int cnt = min(CAP, end - cb);
             double2 acc[Q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                acc[q] = make_double2(0.0, 0.0);
-                const int i = tid + q * G;
-                if (i < cnt) {
-                    const double x = p.xs[cb + i];
-                    const double pr = __dmul_rn(dn, x);
-                    const long long sj = (long long)round(pr);
-                    const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
-                    const long long t = sj & (N - 1);
-                    st2[i] = (int)(t >> p.log_n1);
-                    sh[i] = half_phase(d);
-                }
-            }
+            load_samples<Q, G>(p, cb, cnt, tid, st2, sh, acc);
             for (int r = p.r1 - 1; r >= p.r0; --r) {
-                const double2* row_in = Y + (long long)(r - p.r0) * N + (row << p.log_n2);
-                if (r > p.r0) {
-                    // warm L2 with the next row while this one is transformed
-                    if (tid == 0) {
-                        const void* nxt = Y + (long long)(r - 1 - p.r0) * N + (row << p.log_n2);
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
-                                     "r"((unsigned)(n2 * sizeof(double2))) : "memory");
-                    }
-                }
+                const int ys = p.log_n1 ? 2 : 1;  // element stride of a row in Y
+                const double2* row_in = Y + (p.log_n1 ? y_index(r - p.r0, N, p.log_n2, row, 0)
+                                                      : (long long)(r - p.r0) * N);
                 double2 v[16];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = row_in[tid + q * G];
-                block_fft<L2, -1>(v, buf0, buf1, tid, tw, [] { __syncthreads(); });
+                for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + ys * (tid + q * G));
+                block_fft<L2, -1>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
 #pragma unroll
                 for (int q = 0; q < 16; ++q) xb[tid + q * G] = v[q];
                 __syncthreads();
@@ -252,32 +313,88 @@ __global__ void __launch_bounds__(L2 / 16, 1)
                 }
                 __syncthreads();
             }
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                const int i = tid + q * G;
-                if (i < cnt) {
-                    double2 out = acc[q];
-                    if constexpr (!UNIFORM) {
-                        const double h = sh[i];
-                        if (p.r0 > 0) {  // restore the (i h)^r0 factor of a partial term range
-                            double hr = 1.0;
-                            for (int k = 0; k < p.r0; ++k) hr *= h;
-                            out = cscale(out, hr);
-                            switch (p.r0 & 3) {
-                                case 1: out = make_double2(-out.y, out.x); break;
-                                case 2: out = make_double2(-out.x, -out.y); break;
-                                case 3: out = make_double2(out.y, -out.x); break;
-                                default: break;
-                            }
-                        }
-                        double sn, cs;
-                        sincos(2.0 * h, &sn, &cs);
-                        out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
-                    }
-                    f[p.perm[cb + i]] = out;
-                }
-            }
+            store_samples<Q, G, UNIFORM>(p, cb, cnt, tid, sh, acc, f);
             __syncthreads();
+        }
+    }
+}
+
+// Warp-specialized rows (L2 >= 1024): threads [0, G) run the row FFTs, threads
+// [G, 2G) own the samples.  X_r alternates between two shared buffers; named
+// barriers FULL_b (X ready) and EMPTY_b (samples done) hand buffers back and
+// forth, so the sample warps' Horner updates of step r overlap the FFT of r-1.
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(2 * (L2 / 16), 1)
+    k2_pass2_ws(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
+    constexpr int G = L2 / 16;
+    constexpr int Q = kMaxSamplesPerThread;
+    constexpr int CAP = Q * G;
+    constexpr int ALL = 2 * G;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_FFT = 5;
+    extern __shared__ double2 smem[];
+    double2* bufs = smem;  // 2 x padded_len(L2)
+    double2* t16 = bufs + 2 * padded_len(L2);
+    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::T16_LEN);
+    int* st2 = reinterpret_cast<int*>(sh + CAP);
+    const bool fft_warp = threadIdx.x < G;
+    const int tid = fft_warp ? threadIdx.x : threadIdx.x - G;
+    twiddle_table_build<L2>(t16, threadIdx.x, ALL);
+    Twiddles<L2> T;
+    if (fft_warp) twiddle_init<L2>(T, t16, tid);
+    __syncthreads();
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const long long n2 = 1ll << p.log_n2;
+    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        for (int cb = beg; cb < end; cb += CAP) {
+            const int cnt = min(CAP, end - cb);
+            const int nt = p.r1 - p.r0;
+            if (fft_warp) {
+                for (int i = 0; i < nt; ++i) {
+                    const int r = p.r1 - 1 - i;
+                    const int b = i & 1;
+                    double2* buf = bufs + b * padded_len(L2);
+                    const int rr = r - p.r0;
+                    const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
+                    if (tid == 0 && rr >= 1 && (row & 1) == 0) {  // warm L2: next term's row pair
+                        const void* nxt = Y + y_index(rr - 1, N, p.log_n2, row, 0);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                                     "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
+                    }
+                    double2 v[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    if (i >= 2) nbar_sync(BAR_EMPTY + b, ALL);  // samples done with X_{r+2}
+                    block_fft_1buf<L2, -1>(v, buf, tid, T, [] { nbar_sync(BAR_FFT, G); });
+                    nbar_sync(BAR_FFT, G);  // last-stage reads of buf done
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    nbar_arrive(BAR_FULL + b, ALL);
+                }
+                for (int i = max(0, nt - 2); i < nt; ++i) nbar_sync(BAR_EMPTY + (i & 1), ALL);
+            } else {
+                double2 acc[Q];
+                load_samples<Q, G>(p, cb, cnt, tid, st2, sh, acc);
+                for (int i = 0; i < nt; ++i) {
+                    const int r = p.r1 - 1 - i;
+                    const int b = i & 1;
+                    const double2* xb = bufs + b * padded_len(L2);
+                    nbar_sync(BAR_FULL + b, ALL);
+                    if constexpr (UNIFORM) {
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) {
+                            const int j = tid + q * G;
+                            if (j < cnt) acc[q] = xb[st2[j]];
+                        }
+                    } else {
+                        horner_dispatch<Q, G>(p.deg[r], acc, r, xb, st2, sh, tid, cnt);
+                    }
+                    nbar_arrive(BAR_EMPTY + b, ALL);
+                }
+                store_samples<Q, G, UNIFORM>(p, cb, cnt, tid, sh, acc, f);
+            }
+            __syncthreads();  // st2 / sh / buffers free for the next chunk
         }
     }
 }
@@ -285,16 +402,16 @@ __global__ void __launch_bounds__(L2 / 16, 1)
 // ------------------------------------------------------------------ launch
 template <int L>
 constexpr size_t pass1_smem() {
-    return sizeof(double2) * (L + 2 * padded_len(L) + 16);
+    return sizeof(double2) * (L + 2 * padded_len(L) + 16 + FftShapeX<L>::T16_LEN);
 }
 template <int L>
 constexpr size_t pass2_smem() {
-    return sizeof(double2) * 2 * padded_len(L) + (sizeof(double) + sizeof(int)) * kMaxSamplesPerThread * (L / 16);
+    return sizeof(double2) * (2 * padded_len(L) + FftShapeX<L>::T16_LEN) +
+           (sizeof(double) + sizeof(int)) * kMaxSamplesPerThread * (L / 16);
 }
 
 template <class F>
-void set_smem(F* fn, size_t bytes, int device) {
-    (void)device;
+void set_smem(F* fn, size_t bytes) {
     NB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
@@ -311,17 +428,10 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
     constexpr size_t SM = pass1_smem<L1>();
     Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
     const long long n2 = 1ll << pl.bk.log_n2;
-    if (pl.uniform) {
-        auto fn = k2_pass1<L1, true>;
-        set_smem(fn, SM, pl.device);
-        const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
-        fn<<<grid, L1 / 16, SM, s>>>(c, Y, p, ctx.table(L1));
-    } else {
-        auto fn = k2_pass1<L1, false>;
-        set_smem(fn, SM, pl.device);
-        const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
-        fn<<<grid, L1 / 16, SM, s>>>(c, Y, p, ctx.table(L1));
-    }
+    auto fn = pl.uniform ? k2_pass1<L1, true> : k2_pass1<L1, false>;
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
+    fn<<<grid, L1 / 16, SM, s>>>(c, Y, p);
     NB_LAUNCH();
 }
 
@@ -341,17 +451,13 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
     const long long n1 = 1ll << pl.bk.log_n1;
-    if (pl.uniform) {
-        auto fn = k2_pass2<L2, true>;
-        set_smem(fn, SM, pl.device);
-        const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, L2 / 16, SM));
-        fn<<<grid, L2 / 16, SM, s>>>(Y, f, p, ctx.table(L2));
-    } else {
-        auto fn = k2_pass2<L2, false>;
-        set_smem(fn, SM, pl.device);
-        const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, L2 / 16, SM));
-        fn<<<grid, L2 / 16, SM, s>>>(Y, f, p, ctx.table(L2));
-    }
+    constexpr bool WS = L2 >= 1024;
+    constexpr int threads = WS ? 2 * (L2 / 16) : L2 / 16;
+    auto fn = WS ? (pl.uniform ? k2_pass2_ws<L2, true> : k2_pass2_ws<L2, false>)
+                 : (pl.uniform ? k2_pass2_small<L2, true> : k2_pass2_small<L2, false>);
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, threads, SM));
+    fn<<<grid, threads, SM, s>>>(Y, f, p);
     NB_LAUNCH();
 }
 
