@@ -139,10 +139,11 @@ struct FftShape {
 //  * the Ns = 16 stage uses w_{16 R2}^{k t}, k = j mod 16: a 16 x R2 table in
 //    shared memory laid out [t][k] (one warp load touches 16 consecutive
 //    entries: 2 wavefronts, no conflicts);
-//  * the Ns = 256 stage (L >= 512) uses w_L^{k t} with k = j < 256, i.e. a
-//    per-thread set: bases w^k, w^{2k}, w^{4k}, w^{8k} are evaluated once per
-//    kernel (sincospi, correctly rounded argument) and the other powers are
-//    products of at most three of them (<= ~3 ulp).
+//  * the Ns = 256 stage (L >= 512) uses w_L^{k t} with k = j < 256: bases
+//    w^k, w^{2k}, w^{4k}, w^{8k} live in a [4][256] shared table (evaluated
+//    once per CTA with sincospi, correctly rounded argument; each thread reads
+//    its own column, conflict-free) and the other powers are products of at
+//    most three of them (<= ~3 ulp).
 template <int L>
 struct FftShapeX : FftShape<L> {
     static constexpr int R_LAST = (FftShape<L>::REM > 1) ? FftShape<L>::REM : 16;
@@ -150,38 +151,37 @@ struct FftShapeX : FftShape<L> {
     static constexpr int R3 = (FftShape<L>::STAGES == 3) ? R_LAST : 1;   // radix of the Ns=256 stage
     static constexpr int B3 = 16 / R3;                                    // its butterflies per thread
     static constexpr int T16_LEN = (FftShape<L>::STAGES >= 2) ? 16 * R2 : 16;
+    static constexpr int TB_LEN = (FftShape<L>::STAGES == 3) ? 4 * 256 : 0;  // stage-3 bases
+    static constexpr int TW_LEN = T16_LEN + TB_LEN;  // shared twiddle storage (double2)
 };
 
 template <int L>
 struct Twiddles {
-    using X = FftShapeX<L>;
-    const double2* t16;                       // shared: t16[t*16 + k] = w_{16 R2}^{k t} (forward)
-    double2 b[X::STAGES == 3 ? X::B3 : 1][4];  // stage-3 bases per butterfly: w^k, w^2k, w^4k, w^8k
+    // shared: t16[t*16 + k] = w_{16 R2}^{k t};  tb[e*256 + k] = w_L^{(k 2^e) mod L}, k < 256
+    const double2* t16;
+    const double2* tb;
 };
 
-// fill the Ns=16 table (all threads of the CTA; barrier before use)
+// fill the shared twiddle storage tw (TW_LEN entries; all threads of the
+// CTA, barrier before use)
 template <int L>
-__device__ __forceinline__ void twiddle_table_build(double2* t16, int tid, int nthreads) {
+__device__ __forceinline__ void twiddle_table_build(double2* tw, int tid, int nthreads) {
     using X = FftShapeX<L>;
     for (int i = tid; i < X::T16_LEN; i += nthreads) {
         const int t = i >> 4, k = i & 15;
-        t16[i] = unit_root((long long)k * t, 16 * X::R2);
+        tw[i] = unit_root((long long)k * t, 16 * X::R2);
+    }
+    for (int i = tid; i < X::TB_LEN; i += nthreads) {
+        const long long e = i >> 8, k = i & 255;
+        tw[X::T16_LEN + i] = unit_root((k << e) % L, L);
     }
 }
 
 template <int L>
-__device__ __forceinline__ void twiddle_init(Twiddles<L>& T, const double2* t16, int tid) {
-    using X = FftShapeX<L>;
-    T.t16 = t16;
-    if constexpr (X::STAGES == 3) {
-#pragma unroll
-        for (int bb = 0; bb < X::B3; ++bb) {
-            const long long k = tid + bb * (L / 16);  // j < 256: k = j
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                T.b[bb][e] = (X::R3 > (1 << e)) ? unit_root((k << e) % L, L) : make_double2(1.0, 0.0);
-        }
-    }
+__device__ __forceinline__ void twiddle_init(Twiddles<L>& T, const double2* tw, int tid) {
+    (void)tid;
+    T.t16 = tw;
+    T.tb = tw + FftShapeX<L>::T16_LEN;
 }
 
 template <int SIGN>
@@ -190,26 +190,27 @@ __device__ __forceinline__ double2 tw_sign(double2 w) {
 }
 
 // a[t] *= w^t (t = 1..R-1) for the Ns = 256 stage, powers from the bases
+// bs[e*256] = w^(k 2^e) (shared, per-thread column k)
 template <int R, int SIGN>
-__device__ __forceinline__ void apply_pow_twiddles(double2* a, const double2 (&bs)[4]) {
+__device__ __forceinline__ void apply_pow_twiddles(double2* a, const double2* bs) {
     const double2 p1 = tw_sign<SIGN>(bs[0]);
     if constexpr (R == 2) {
         a[1] = cmul(a[1], p1);
     } else {
-        const double2 p2 = tw_sign<SIGN>(bs[1]);
+        const double2 p2 = tw_sign<SIGN>(bs[256]);
         const double2 p3 = cmul(p1, p2);
         a[1] = cmul(a[1], p1);
         a[2] = cmul(a[2], p2);
         a[3] = cmul(a[3], p3);
         if constexpr (R >= 8) {
-            const double2 p4 = tw_sign<SIGN>(bs[2]);
+            const double2 p4 = tw_sign<SIGN>(bs[512]);
             const double2 p5 = cmul(p1, p4), p6 = cmul(p2, p4), p7 = cmul(p3, p4);
             a[4] = cmul(a[4], p4);
             a[5] = cmul(a[5], p5);
             a[6] = cmul(a[6], p6);
             a[7] = cmul(a[7], p7);
             if constexpr (R == 16) {
-                const double2 p8 = tw_sign<SIGN>(bs[3]);
+                const double2 p8 = tw_sign<SIGN>(bs[768]);
                 a[8] = cmul(a[8], p8);
                 a[9] = cmul(a[9], cmul(p1, p8));
                 a[10] = cmul(a[10], cmul(p2, p8));
@@ -242,7 +243,7 @@ __device__ __forceinline__ void stockham_stage(double2 (&v)[16], double2* out, i
 #pragma unroll
             for (int t = 1; t < R; ++t) a[t] = cmul(a[t], tw_sign<SIGN>(T.t16[t * 16 + k]));
         } else if constexpr (NS == 256) {
-            apply_pow_twiddles<R, SIGN>(a, T.b[b]);
+            apply_pow_twiddles<R, SIGN>(a, T.tb + k);
         } else {
             static_assert(NS == 1, "stage");
         }

@@ -55,7 +55,7 @@ constexpr int block_groups() {
 }
 template <int L>
 constexpr size_t block_smem() {
-    return sizeof(double2) * (2 * padded_len(L) * block_groups<L>() + FftShapeX<L>::T16_LEN);
+    return sizeof(double2) * (2 * padded_len(L) * block_groups<L>() + FftShapeX<L>::TW_LEN);
 }
 
 template <int L, int SIGN>

@@ -6,15 +6,15 @@
 // (accumulate_term :152-161).  Here the K terms are fused into two passes of
 // a four-step FFT, N = N1 * N2 (k = k1*N2 + k2, t = t1 + N1*t2):
 //
-//  pass 1 (CTA per column k2, persistent, two CTAs per SM): for every r the
-//    column c[k1*N2 + k2] is read (from HBM once, then L2), scaled by
-//    v_r = T_r(2k/N - 1) (Chebyshev recurrence evaluated in registers), the
-//    N1-point column FFT runs in registers + one shared exchange buffer, the
+//  pass 1 (CTA per column k2, persistent): the column c[k1*N2 + k2] is read
+//    from HBM once into shared memory; for every r it is scaled by
+//    v_r = T_r(2k/N - 1) (Chebyshev recurrence state in registers), the
+//    N1-point column FFT runs in registers + shared exchange buffers, the
 //    inter-pass twiddle w_N^{t1 k2} is applied and Y_r[t1][k2] is written
-//    (the only HBM round trip of the K spectra).
+//    (the only HBM round trip of the K spectra; full-sector stores, see y_index).
 //  pass 2 (CTA per row t1, persistent, warp-specialized): FFT warps transform
 //    Y_r[t1][:] for r = K-1 .. 0 into X_r[t1 + N1 t2] (double-buffered shared
-//    memory); sample warps, overlapped one r behind, gather X_r[t2_j] for every
+//    memory); sample warps (1.5x as many), overlapped one r behind, gather X_r[t2_j] for every
 //    sample bucketed on this row (t_j mod N1 == t1, plan-time sort) into a
 //    per-sample register accumulator by Horner in r,
 //        acc <- acc * (i h_j) + g_r(h_j^2) X_r[t2_j],
@@ -25,6 +25,8 @@
 // and read once) — SURVEY.md §8(d).  No atomics: every f[j] is owned by one
 // thread and sums run in a fixed order, so results are bit-reproducible.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "bessel.cuh"
 #include "fft_block.cuh"
@@ -179,36 +181,49 @@ struct Pass2Params {
     const double* xs;
     const int* perm;
     const int* rowoff;
+    unsigned long long* trace;  // diagnostics: per-iteration clock64 stamps of CTA 0 (nullptr = off)
     int deg[kRankCap];
 };
+#define NB_TRACE(slot)                                                                   \
+    do {                                                                                 \
+        if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[(slot)] = clock64();           \
+    } while (0)
 
-template <int D, int Q, int G>
-__device__ __forceinline__ void horner_update(double2 (&acc)[Q], int r, const double2* xb,
-                                              const int* st2, const double* sh, int tid, int cnt) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const int i = tid + q * G;
-        if (i < cnt) {
-            const double h = sh[i];
-            const double2 X = xb[st2[i]];
-            const double g = bessel_g<D>(r, h * h);
-            const double ax = acc[q].x;
-            acc[q].x = __fma_rn(g, X.x, -h * acc[q].y);
-            acc[q].y = __fma_rn(g, X.y, h * ax);
-        }
-    }
-}
-
+// One Horner step in r for the thread's samples: acc <- acc*(i h) + g_r(h^2) X_r[t2].
+// Samples go in chunks of C: the degree-`deg` series for g_r runs as one
+// runtime loop whose coefficient (uniform, constant bank) feeds C independent
+// FMAs; acc stays in registers (the chunk loop is unrolled).
 template <int Q, int G>
-__device__ __forceinline__ void horner_dispatch(int deg, double2 (&acc)[Q], int r, const double2* xb,
-                                                const int* st2, const double* sh, int tid, int cnt) {
-    switch (deg) {
-#define NB_CASE(D) \
-    case D: horner_update<D, Q, G>(acc, r, xb, st2, sh, tid, cnt); break;
-        NB_CASE(0) NB_CASE(1) NB_CASE(2) NB_CASE(3) NB_CASE(4) NB_CASE(5) NB_CASE(6) NB_CASE(7)
-        NB_CASE(8) NB_CASE(9) NB_CASE(10) NB_CASE(11) NB_CASE(12) NB_CASE(13) NB_CASE(14)
-        default: horner_update<15, Q, G>(acc, r, xb, st2, sh, tid, cnt); break;
-#undef NB_CASE
+__device__ __forceinline__ void horner_step(double2 (&acc)[Q], int r, int deg, const double2* xb,
+                                            const int* st2, const double* sh, int tid, int cnt) {
+    constexpr int C = 4;
+    const double* a = kBes + r * kSeriesTerms;
+#pragma unroll
+    for (int q0 = 0; q0 < Q; q0 += C) {
+        double h[C], w[C], g[C];
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const int i = tid + (q0 + u) * G;
+            h[u] = (q0 + u < Q && i < cnt) ? sh[i] : 0.0;
+            w[u] = h[u] * h[u];
+            g[u] = 0.0;
+        }
+        for (int m = deg; m >= 0; --m) {
+            const double am = a[m];
+#pragma unroll
+            for (int u = 0; u < C; ++u) g[u] = __fma_rn(g[u], w[u], am);
+        }
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const int q = q0 + u;
+            const int i = tid + q * G;
+            if (q < Q && i < cnt) {
+                const double2 X = xb[st2[i]];
+                const double ax = acc[q].x;
+                acc[q].x = __fma_rn(g[u], X.x, -h[u] * acc[q].y);
+                acc[q].y = __fma_rn(g[u], X.y, h[u] * ax);
+            }
+        }
     }
 }
 
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(L2 / 16)
     double2* buf0 = smem;
     double2* buf1 = buf0 + padded_len(L2);
     double2* t16 = buf1 + padded_len(L2);
-    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::T16_LEN);
+    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::TW_LEN);
     int* st2 = reinterpret_cast<int*>(sh + CAP);
     const int tid = threadIdx.x;
     twiddle_table_build<L2>(t16, tid, G);
@@ -309,7 +324,7 @@ __global__ void __launch_bounds__(L2 / 16)
                         if (i < cnt) acc[q] = xb[st2[i]];
                     }
                 } else {
-                    horner_dispatch<Q, G>(p.deg[r], acc, r, xb, st2, sh, tid, cnt);
+                    horner_step<Q, G>(acc, r, p.deg[r], xb, st2, sh, tid, cnt);
                 }
                 __syncthreads();
             }
@@ -319,29 +334,82 @@ __global__ void __launch_bounds__(L2 / 16)
     }
 }
 
+// mbarrier helpers (shared::cta)
+__device__ __forceinline__ void mbar_init(unsigned long long* m, int count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, int parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+// async arrive when this thread's prior cp.async operations have completed
+__device__ __forceinline__ void mbar_cp_async_arrive(unsigned long long* m) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gsrc) : "memory");
+}
+
 // Warp-specialized rows (L2 >= 1024): threads [0, G) run the row FFTs, threads
-// [G, 2G) own the samples.  X_r alternates between two shared buffers; named
-// barriers FULL_b (X ready) and EMPTY_b (samples done) hand buffers back and
-// forth, so the sample warps' Horner updates of step r overlap the FFT of r-1.
-template <int L2, bool UNIFORM>
-__global__ void __launch_bounds__(2 * (L2 / 16), 1)
+// [G, 2G) own the samples.  X_r alternates between two shared buffers.
+//   FULL_b (named barrier): X_r is in buffer b -> sample warps may gather.
+//   staged_b (mbarrier):    sample warps finished with buffer b and the
+//                           Y row of term r-2 has landed in it (cp.async
+//                           issued by the sample warps, completion tracked
+//                           asynchronously) -> FFT warps may start FFT(r-2).
+// The sample warps' Horner updates of step r and the staging copy overlap
+// the FFT of r-1; no warp blocks on a global load except the first two rows
+// of a chunk.
+// Sample role width: S = 1.5 G threads holding QS = 12 samples each
+// (capacity 18 G = 1.125 N2, above the Poisson spread of an iid row): more
+// warps than the FFT role, because the per-term sample update is a chain of
+// dependent shared loads and FMAs that needs many warps in flight.
+template <int L2, int X2>
+struct WsShape {
+    static constexpr int G = L2 / 16;   // FFT role threads
+    static constexpr int S = G * X2 / 2;  // sample role threads (X2 = 2: as many as the FFT role)
+    static constexpr int QS = (18 * G + S - 1) / S;          // samples per sample thread
+    static constexpr int CAP = QS * S;  // samples per chunk
+    static constexpr int ALL = G + S;
+};
+
+template <int L2, bool UNIFORM, int X2, bool STAGE>
+__global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
     k2_pass2_ws(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
-    constexpr int G = L2 / 16;
-    constexpr int Q = kMaxSamplesPerThread;
-    constexpr int CAP = Q * G;
-    constexpr int ALL = 2 * G;
-    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_FFT = 5;
+    using W = WsShape<L2, X2>;
+    constexpr int G = W::G;
+    constexpr int S = W::S;
+    constexpr int Q = W::QS;
+    constexpr int CAP = W::CAP;
+    constexpr int ALL = W::ALL;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_FFT = 5, BAR_SMP = 6;
     extern __shared__ double2 smem[];
+    __shared__ unsigned long long staged[2];
     double2* bufs = smem;  // 2 x padded_len(L2)
     double2* t16 = bufs + 2 * padded_len(L2);
-    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::T16_LEN);
+    double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::TW_LEN);
     int* st2 = reinterpret_cast<int*>(sh + CAP);
     const bool fft_warp = threadIdx.x < G;
     const int tid = fft_warp ? threadIdx.x : threadIdx.x - G;
     twiddle_table_build<L2>(t16, threadIdx.x, ALL);
     Twiddles<L2> T;
     if (fft_warp) twiddle_init<L2>(T, t16, tid);
+    if (threadIdx.x == 0) {
+        mbar_init(&staged[0], S);
+        mbar_init(&staged[1], S);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
+    int phase[2] = {0, 0};  // completed stagings per buffer (identical in both roles)
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
     const long long n2 = 1ll << p.log_n2;
@@ -356,43 +424,73 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
                     const int b = i & 1;
                     double2* buf = bufs + b * padded_len(L2);
                     const int rr = r - p.r0;
-                    const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
-                    if (tid == 0 && rr >= 1 && (row & 1) == 0) {  // warm L2: next term's row pair
-                        const void* nxt = Y + y_index(rr - 1, N, p.log_n2, row, 0);
+                    if (tid == 0 && rr >= 2 && (row & 1) == 0) {  // warm L2 for the staging copy
+                        const void* nxt = Y + y_index(rr - 2, N, p.log_n2, row, 0);
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
                                      "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
                     }
                     double2 v[16];
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 0);
+                    if (!STAGE) {
+                        const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
-                    if (i >= 2) nbar_sync(BAR_EMPTY + b, ALL);  // samples done with X_{r+2}
+                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                        if (i >= 2) nbar_sync(BAR_EMPTY + b, ALL);  // samples done with X_{r+2}
+                    } else if (i >= 2) {
+                        mbar_wait(&staged[b], phase[b] & 1);
+                        ++phase[b];
+                        load_stage_input<L2>(v, buf, tid);
+                        nbar_sync(BAR_FFT, G);  // all inputs read before stage 1 reuses buf
+                    } else {
+                        const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    }
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 1);
                     block_fft_1buf<L2, -1>(v, buf, tid, T, [] { nbar_sync(BAR_FFT, G); });
                     nbar_sync(BAR_FFT, G);  // last-stage reads of buf done
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 2);
                     nbar_arrive(BAR_FULL + b, ALL);
                 }
-                for (int i = max(0, nt - 2); i < nt; ++i) nbar_sync(BAR_EMPTY + (i & 1), ALL);
+                if (!STAGE)
+                    for (int i = max(0, nt - 2); i < nt; ++i) nbar_sync(BAR_EMPTY + (i & 1), ALL);
             } else {
                 double2 acc[Q];
-                load_samples<Q, G>(p, cb, cnt, tid, st2, sh, acc);
+                load_samples<Q, S>(p, cb, cnt, tid, st2, sh, acc);
                 for (int i = 0; i < nt; ++i) {
                     const int r = p.r1 - 1 - i;
                     const int b = i & 1;
-                    const double2* xb = bufs + b * padded_len(L2);
+                    double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, ALL);
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 4);
                     if constexpr (UNIFORM) {
 #pragma unroll
                         for (int q = 0; q < Q; ++q) {
-                            const int j = tid + q * G;
+                            const int j = tid + q * S;
                             if (j < cnt) acc[q] = xb[st2[j]];
                         }
                     } else {
-                        horner_dispatch<Q, G>(p.deg[r], acc, r, xb, st2, sh, tid, cnt);
+                        horner_step<Q, S>(acc, r, p.deg[r], xb, st2, sh, tid, cnt);
                     }
-                    nbar_arrive(BAR_EMPTY + b, ALL);
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 5);
+                    if (!STAGE) {
+                        nbar_arrive(BAR_EMPTY + b, ALL);
+                    } else if (i + 2 < nt) {  // stage the Y row of term r-2 into this buffer
+                        nbar_sync(BAR_SMP, S);  // every sample warp is done reading X_r here
+                        const double2* src = Y + y_index(r - 2 - p.r0, N, p.log_n2, row, 0);
+#pragma unroll
+                        for (int q = 0; q < L2 / S; ++q) {
+                            const int k2 = tid + q * S;
+                            cp_async16(xb + pad16(k2), src + 2 * k2);
+                        }
+                        mbar_cp_async_arrive(&staged[b]);
+                        ++phase[b];
+                    }
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 6);
                 }
-                store_samples<Q, G, UNIFORM>(p, cb, cnt, tid, sh, acc, f);
+                store_samples<Q, S, UNIFORM>(p, cb, cnt, tid, sh, acc, f);
             }
             __syncthreads();  // st2 / sh / buffers free for the next chunk
         }
@@ -402,12 +500,13 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
 // ------------------------------------------------------------------ launch
 template <int L>
 constexpr size_t pass1_smem() {
-    return sizeof(double2) * (L + 2 * padded_len(L) + 16 + FftShapeX<L>::T16_LEN);
+    return sizeof(double2) * (L + 2 * padded_len(L) + 16 + FftShapeX<L>::TW_LEN);
 }
-template <int L>
+template <int L, int X2 = 2>
 constexpr size_t pass2_smem() {
-    return sizeof(double2) * (2 * padded_len(L) + FftShapeX<L>::T16_LEN) +
-           (sizeof(double) + sizeof(int)) * kMaxSamplesPerThread * (L / 16);
+    constexpr int cap = (L >= 1024) ? WsShape<L, X2>::CAP : kMaxSamplesPerThread * (L / 16);
+    return sizeof(double2) * (2 * padded_len(L) + FftShapeX<L>::TW_LEN) +
+           (sizeof(double) + sizeof(int)) * cap;
 }
 
 template <class F>
@@ -435,11 +534,34 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
     NB_LAUNCH();
 }
 
+// pass-2 organization for rows >= 1024 (sample-role width X2/2 of the FFT
+// role, Y staging on/off); NUFFT_PASS2_VARIANT selects one for experiments
+// (0: X2=2 no staging, 1: X2=2 staged, 2: X2=3 no staging [default],
+//  3: X2=3 staged) — measured on B200 at N=2^24: 3.45 / 4.41 / 3.36 / 3.89 ms
+inline int pass2_variant() {
+    static const int v = [] {
+        const char* e = getenv("NUFFT_PASS2_VARIANT");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
+template <int L2, bool UNIFORM, int X2, bool STAGE>
+void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms,
+               cudaStream_t s) {
+    constexpr size_t SM = pass2_smem<L2, X2>();
+    constexpr int threads = WsShape<L2, X2>::ALL;
+    auto fn = k2_pass2_ws<L2, UNIFORM, X2, STAGE>;
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
+    fn<<<grid, threads, SM, s>>>(Y, f, p);
+    NB_LAUNCH();
+}
+
 template <int L2>
 void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int r1,
                   cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
-    constexpr size_t SM = pass2_smem<L2>();
     Pass2Params p{};
     p.n = (long long)pl.n;
     p.log_n1 = pl.bk.log_n1;
@@ -450,15 +572,46 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.perm = pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
+    static const bool trace = getenv("NUFFT_TRACE_PASS2") != nullptr;
+    unsigned long long* tr = nullptr;
+    if (trace) {
+        NB_CUDA(cudaMalloc(&tr, 8 * 8 * 64));
+        NB_CUDA(cudaMemset(tr, 0, 8 * 8 * 64));
+    }
+    p.trace = tr;
     const long long n1 = 1ll << pl.bk.log_n1;
-    constexpr bool WS = L2 >= 1024;
-    constexpr int threads = WS ? 2 * (L2 / 16) : L2 / 16;
-    auto fn = WS ? (pl.uniform ? k2_pass2_ws<L2, true> : k2_pass2_ws<L2, false>)
-                 : (pl.uniform ? k2_pass2_small<L2, true> : k2_pass2_small<L2, false>);
-    set_smem(fn, SM);
-    const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, threads, SM));
-    fn<<<grid, threads, SM, s>>>(Y, f, p);
-    NB_LAUNCH();
+    if constexpr (L2 >= 1024) {
+        const bool u = pl.uniform;
+        switch (pass2_variant()) {
+            case 1: u ? launch_ws<L2, true, 2, true>(Y, f, p, n1, ctx.sms, s)
+                      : launch_ws<L2, false, 2, true>(Y, f, p, n1, ctx.sms, s); break;
+            case 2: u ? launch_ws<L2, true, 3, false>(Y, f, p, n1, ctx.sms, s)
+                      : launch_ws<L2, false, 3, false>(Y, f, p, n1, ctx.sms, s); break;
+            case 3: u ? launch_ws<L2, true, 3, true>(Y, f, p, n1, ctx.sms, s)
+                      : launch_ws<L2, false, 3, true>(Y, f, p, n1, ctx.sms, s); break;
+            default: u ? launch_ws<L2, true, 2, false>(Y, f, p, n1, ctx.sms, s)
+                       : launch_ws<L2, false, 2, false>(Y, f, p, n1, ctx.sms, s); break;
+        }
+    } else {
+        constexpr size_t SM = pass2_smem<L2>();
+        constexpr int threads = L2 / 16;
+        auto fn = pl.uniform ? k2_pass2_small<L2, true> : k2_pass2_small<L2, false>;
+        set_smem(fn, SM);
+        const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, threads, SM));
+        fn<<<grid, threads, SM, s>>>(Y, f, p);
+        NB_LAUNCH();
+    }
+    if (tr) {
+        unsigned long long h[8 * 64];
+        NB_CUDA(cudaStreamSynchronize(s));
+        NB_CUDA(cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost));
+        const unsigned long long t0 = h[0];
+        for (int i = 0; i < r1 - r0; ++i)
+            fprintf(stderr, "trace i=%2d fft[start %7lld input %7lld done %7lld]  smp[full %7lld horner %7lld staged %7lld]\n", i,
+                    (long long)(h[8 * i] - t0), (long long)(h[8 * i + 1] - t0), (long long)(h[8 * i + 2] - t0),
+                    (long long)(h[8 * i + 4] - t0), (long long)(h[8 * i + 5] - t0), (long long)(h[8 * i + 6] - t0));
+        cudaFree(tr);
+    }
 }
 
 void dispatch_pass1(int L, const double2* c, double2* Y, const CorePlan& pl, int r0, int r1,
