@@ -93,6 +93,7 @@ void conj_copy(const double2* in, double2* out, size_t n, cudaStream_t s) {
 
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
                     cudaStream_t s) {
+    if (p.fused) return exec_transpose_fused(p, g, f, batch, s);
     ensure_bessel_constants(p.device);
     if (!p.have_bins) throw Error(kInternal, "transpose core: plan has no bins");
     const size_t N = p.n;

@@ -303,8 +303,10 @@ void build_buckets(CorePlan& p, cudaStream_t s) {
     }
     p.bk.log_n1 = log_n1;
     p.bk.log_n2 = log_n2;
-    DevBuf keys(4 * n, s), keys_out(4 * n, s), idx(4 * n, s);
+    DevBuf keys(4 * n, s), idx(4 * n, s);
     p.bk.perm.alloc(4 * n);
+    p.bk.skey.alloc(4 * n);
+    DevArray& keys_out = p.bk.skey;
     k_bucket_keys<<<blocks(n), 256, 0, s>>>(p.ax.t.as<long long>(), (long long)n, log_n1, log_n2,
                                             keys.as<unsigned>(), idx.as<int>());
     NB_LAUNCH();
@@ -324,6 +326,10 @@ void build_buckets(CorePlan& p, cudaStream_t s) {
     p.bk.xs.alloc(8 * n);
     k_gather_x<<<blocks(n), 256, 0, s>>>(p.ax.x.as<double>(), p.bk.perm.as<int>(), (long long)n,
                                          p.bk.xs.as<double>());
+    NB_LAUNCH();
+    p.bk.ds.alloc(8 * n);
+    k_gather_x<<<blocks(n), 256, 0, s>>>(p.ax.delta.as<double>(), p.bk.perm.as<int>(), (long long)n,
+                                         p.bk.ds.as<double>());
     NB_LAUNCH();
 }
 

@@ -9,6 +9,8 @@
 //   xs     x sorted by (t mod N1, t div N1)         fp64   [8]
 //   perm   original index of each sorted sample     int32  [4]
 //   rowoff N1+1 bucket offsets                       int32
+//   ds     delta sorted like xs (transpose core)      fp64   [8]
+//   skey   sorted bucket key (t1 << log2 N2) | t2     uint32 [4]
 // The exec kernels read only xs + perm (12 B/sample) and recompute s, t,
 // delta from x exactly as the reference does (transforms.hpp:60-64,84-86).
 #pragma once
@@ -36,6 +38,7 @@ struct Axis {
 struct Buckets {
     int log_n1 = 0, log_n2 = 0;  // N = N1*N2
     DevArray xs, perm, rowoff;   // see header comment
+    DevArray ds, skey;           // fused transpose core (type I / adjoint / III inner)
     DevArray sort_perm;          // generic transpose core: samples sorted by t (int32)
     DevArray bin_off;            // generic transpose core: N+1 offsets (int32)
 };
@@ -99,6 +102,10 @@ void exec_type2(const CorePlan& p, const double2* c, double2* f, size_t batch, s
 // F2~^T g = sum_r v_r .* F scatter_t(u_r .* g)   (transforms.hpp:206-221)
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
                     cudaStream_t s);
+// fused two-pass form of exec_transpose for power-of-two N (transpose_fused.cu);
+// ev as for exec_type2
+void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_t batch,
+                          cudaStream_t s, cudaEvent_t* ev = nullptr);
 void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s);

@@ -1,0 +1,416 @@
+// Fused transpose core (type I, the type-II adjoint, type-III inner stage).
+//
+// Reference: exec_transpose_core transforms.hpp:206-221
+//   F2~^T g = sum_r v_r .* F scatter_t(u_r .* g)     (F symmetric: F^T = F)
+// evaluated by the reference as K passes of {scale, scatter, FFTW, scale-add}
+// over HBM-sized vectors.  Here the K terms run in two passes of a four-step
+// FFT, N = N1*N2, bins t = t1 + N1 t2, outputs k = k1 N2 + k2 — the mirror
+// image of the type-II kernels (nufft2.cu):
+//
+//  pass A (CTA per row t1, persistent): the samples bucketed on the row
+//    (plan-time sort by (t1, t2), ascending j inside a bin) are staged once
+//    per row in shared memory as G_j = 2 exp(2 i h_j) g_j and h_j.  For every
+//    r, a term phase (each thread owns 17 samples: balanced, branch-free,
+//    17 independent Horner chains per Bessel coefficient) writes
+//        T_j = (h_j^r g_r(h_j^2)) G_j            (= i^-r u_r[j] g_j, bessel.cuh)
+//    into the idle FFT exchange buffer; a bin phase sums each of the thread's
+//    16 bins in ascending j (the reference's order; no atomics); then the
+//    N2-point row FFT runs in registers + shared memory, i^r is applied and
+//    Z_r[t1][k2] is written (row-major, full-sector stores).
+//  pass B (CTA per column k2, persistent): for r = 0..K-1 the column
+//    Z_r[:][k2] is read, multiplied by the inter-pass twiddle w_N^{t1 k2},
+//    transformed (N1-point FFT) and accumulated into registers as
+//    acc[k] += v_r(k) X_r[k] with the Chebyshev recurrence for v_r; f is
+//    written once.
+//
+// HBM bytes per point (batch 1): g 16 (gathered) + f 16 + delta/key/perm 16
+// + 32 K (Z written and read once).
+#include <algorithm>
+
+#include "bessel.cuh"
+#include "fft_block.cuh"
+#include "plans.hpp"
+
+namespace nb {
+
+namespace {
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+struct PassAParams {
+    long long n;
+    int log_n1, log_n2;
+    int r0, r1;
+    const double* ds;
+    const unsigned* skey;
+    const int* perm;
+    const int* rowoff;
+    int deg[kRankCap];
+};
+
+struct PassBParams {
+    long long n;
+    int log_n1, log_n2;
+    int r0, r1;
+};
+
+// multiply by i^r
+__device__ __forceinline__ double2 rot_ipow(double2 z, int r) {
+    switch (r & 3) {
+        case 1: return make_double2(-z.y, z.x);
+        case 2: return make_double2(-z.x, -z.y);
+        case 3: return make_double2(z.y, -z.x);
+        default: return z;
+    }
+}
+
+// samples per chunk of a row in pass A and the shared-memory footprint.  The
+// per-term sample products are staged in the FFT exchange buffer (it is idle
+// between two transforms), so a chunk holds at most padded_len(L2) = 17 G
+// samples: QA = 17 per thread, a fixed, fully unrolled count.
+template <int L2>
+struct PassAShape {
+    static constexpr int G = L2 / 16;
+    static constexpr int QA = 17;
+    static constexpr int CAP = QA * G;  // == padded_len(L2)
+    static constexpr size_t SMEM = sizeof(double2) * (padded_len(L2) + FftShapeX<L2>::TW_LEN) +
+                                   (sizeof(double2) + sizeof(double)) * CAP + sizeof(unsigned) * L2;
+    static_assert(CAP == padded_len(L2) && CAP <= 65535, "pass A capacity");
+    static_assert(SMEM <= kSmemLimit, "pass A shared memory");
+};
+
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(L2 / 16, 1)
+    k1_passA(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p) {
+    using S = PassAShape<L2>;
+    constexpr int G = S::G;
+    constexpr int QA = S::QA;
+    constexpr int CAP = S::CAP;
+    extern __shared__ double2 smem[];
+    double2* buf = smem;  // FFT exchange buffer; holds the sample terms between transforms
+    double2* tw = buf + padded_len(L2);
+    double2* gs = tw + FftShapeX<L2>::TW_LEN;
+    double* hs = reinterpret_cast<double*>(gs + CAP);
+    unsigned* bo = reinterpret_cast<unsigned*>(hs + CAP);  // bin b: [lo16, hi16) of the chunk
+    unsigned short* bo16 = reinterpret_cast<unsigned short*>(bo);
+    const int tid = threadIdx.x;
+    twiddle_table_build<L2>(tw, tid, G);
+    Twiddles<L2> T;
+    twiddle_init<L2>(T, tw, tid);
+    __syncthreads();
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const unsigned mask = (1u << p.log_n2) - 1u;
+    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        if (beg == end) {  // empty row: Z_r[row][:] = 0
+            for (int r = p.r0; r < p.r1; ++r) {
+                double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) out[tid + q * G] = make_double2(0.0, 0.0);
+            }
+            continue;
+        }
+        for (int cb = beg, chunk = 0; cb < end; cb += CAP, ++chunk) {
+            const int cnt = min(CAP, end - cb);
+            for (int i = tid; i < L2; i += G) bo[i] = 0u;
+            __syncthreads();
+            for (int i = tid; i < cnt; i += G) {
+                const unsigned t2 = p.skey[cb + i] & mask;
+                if (i == 0 || (p.skey[cb + i - 1] & mask) != t2) bo16[2 * t2] = (unsigned short)i;
+                if (i == cnt - 1 || (p.skey[cb + i + 1] & mask) != t2) bo16[2 * t2 + 1] = (unsigned short)(i + 1);
+                const double2 gv = __ldg(g + p.perm[cb + i]);
+                if constexpr (UNIFORM) {
+                    gs[i] = gv;
+                } else {
+                    const double h = half_phase(p.ds[cb + i]);
+                    double sn, cs;
+                    sincos(2.0 * h, &sn, &cs);
+                    hs[i] = h;
+                    gs[i] = cmul(make_double2(2.0 * cs, 2.0 * sn), gv);
+                }
+            }
+            for (int i = cnt + tid; i < CAP; i += G) {  // tail slots: zero terms
+                gs[i] = make_double2(0.0, 0.0);
+                if constexpr (!UNIFORM) hs[i] = 0.0;
+            }
+            double hr[QA];  // h^r of the thread's samples tid + u G (fixed ownership)
+#pragma unroll
+            for (int u = 0; u < QA; ++u) hr[u] = 1.0;
+            __syncthreads();
+            if constexpr (!UNIFORM) {
+                for (int r = 0; r < p.r0; ++r) {
+#pragma unroll
+                    for (int u = 0; u < QA; ++u) hr[u] *= hs[tid + u * G];
+                }
+            }
+            for (int r = p.r0; r < p.r1; ++r) {
+                __syncthreads();  // previous term's last-stage reads of buf are done
+                const double2* src = gs;
+                if constexpr (!UNIFORM) {
+                    // term phase: buf[i] = h_i^r g_r(h_i^2) G_i (every thread QA samples)
+                    const double* a = kBes + r * kSeriesTerms;
+                    const int deg = p.deg[r];
+                    double w[QA], gr[QA];
+#pragma unroll
+                    for (int u = 0; u < QA; ++u) {
+                        const double h = hs[tid + u * G];
+                        w[u] = h * h;
+                        gr[u] = 0.0;
+                    }
+                    for (int m = deg; m >= 0; --m) {
+                        const double am = a[m];
+#pragma unroll
+                        for (int u = 0; u < QA; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
+                    }
+#pragma unroll
+                    for (int u = 0; u < QA; ++u) {
+                        const int i = tid + u * G;
+                        const double m = hr[u] * gr[u];
+                        buf[i] = cscale(gs[i], m);
+                        hr[u] *= hs[i];
+                    }
+                    src = buf;
+                    __syncthreads();
+                }
+                // bin phase: the thread's 16 bins, duplicates summed in ascending j
+                double2 v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const unsigned rb = bo[tid + q * G];
+                    const int i0 = rb & 0xffffu, i1 = rb >> 16;
+                    double2 acc = make_double2(0.0, 0.0);
+                    if (i0 < i1) {
+                        acc = src[i0];
+                        for (int i = i0 + 1; i < i1; ++i) acc = cadd(acc, src[i]);
+                    }
+                    v[q] = acc;
+                }
+                if constexpr (!UNIFORM) __syncthreads();  // terms read before stage 1 reuses buf
+                block_fft_1buf<L2, -1>(v, buf, tid, T, [] { __syncthreads(); });
+                double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double2 z = UNIFORM ? v[q] : rot_ipow(v[q], r);
+                    const int k2 = tid + q * G;
+                    out[k2] = chunk == 0 ? z : cadd(out[k2], z);
+                }
+            }
+            __syncthreads();  // gs / hs / bins free for the next chunk
+        }
+    }
+}
+
+// pass B: column k2 of every Z_r, inter-pass twiddle, N1-point FFT, v_r accumulate
+template <int L1, bool UNIFORM>
+__global__ void __launch_bounds__(L1 / 16, 1)
+    k1_passB(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p) {
+    constexpr int G = L1 / 16;
+    extern __shared__ double2 smem[];
+    double2* buf0 = smem;
+    double2* buf1 = buf0 + padded_len(L1);
+    double2* step = buf1 + padded_len(L1);
+    double2* tw = step + 16;
+    const int tid = threadIdx.x;
+    twiddle_table_build<L1>(tw, tid, G);
+    Twiddles<L1> T;
+    twiddle_init<L1>(T, tw, tid);
+    const long long n2 = 1ll << p.log_n2;
+    const long long N = p.n;
+    for (long long k2 = blockIdx.x; k2 < n2; k2 += gridDim.x) {
+        __syncthreads();  // previous column's readers of step are done
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
+        const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
+        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+        double tcur[16], tprev[16];
+        double2 acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            acc[q] = make_double2(0.0, 0.0);
+            tprev[q] = 1.0;
+            tcur[q] = 0.5 * (two_s0 + 0.25 * q);
+        }
+        if constexpr (!UNIFORM) {
+            for (int r = 1; r < p.r0; ++r) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                    tprev[q] = tcur[q];
+                    tcur[q] = tn;
+                }
+            }
+        }
+        __syncthreads();
+        for (int r = p.r0; r < p.r1; ++r) {
+            if constexpr (FftShape<L1>::STAGES < 3) __syncthreads();  // buf0 reuse across r
+            const double2* col = Z + (long long)(r - p.r0) * N + k2;
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const long long t1 = tid + q * G;
+                v[q] = cmul(__ldcg(col + (t1 << p.log_n2)), cmul(base, step[q]));
+            }
+            block_fft<L1, -1>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                if constexpr (UNIFORM) {
+                    acc[q] = cadd(acc[q], v[q]);
+                } else {
+                    const double vr = (r == 0) ? 0.5 : tcur[q];
+                    acc[q].x = __fma_rn(vr, v[q].x, acc[q].x);
+                    acc[q].y = __fma_rn(vr, v[q].y, acc[q].y);
+                }
+            }
+            if constexpr (!UNIFORM) {
+                if (r > 0) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                        tprev[q] = tcur[q];
+                        tcur[q] = tn;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const long long k1 = tid + q * G;
+            f[(k1 << p.log_n2) + k2] = acc[q];
+        }
+    }
+}
+
+// N1 == 1: f[k] = sum_r v_r(k) Z_r[k]
+__global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ f, long long N,
+                           int r0, int r1, int uniform) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const double s = __dsub_rn(__dmul_rn(2.0, (double)k / (double)N), 1.0);
+    double tprev = 1.0, tcur = s;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int r = 0; r < r1; ++r) {
+        double vr;
+        if (r == 0) {
+            vr = 0.5;
+        } else {
+            if (r >= 2) {
+                const double tn = __fma_rn(2.0 * s, tcur, -tprev);
+                tprev = tcur;
+                tcur = tn;
+            }
+            vr = tcur;
+        }
+        if (r < r0) continue;
+        const double2 z = Z[(long long)(r - r0) * N + k];
+        if (uniform) {
+            acc = cadd(acc, z);
+        } else {
+            acc.x = __fma_rn(vr, z.x, acc.x);
+            acc.y = __fma_rn(vr, z.y, acc.y);
+        }
+    }
+    f[k] = acc;
+}
+
+template <class F>
+void set_smem(F* fn, size_t bytes) {
+    NB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+int occupancy(const void* fn, int threads, size_t smem) {
+    int n = 0;
+    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    return std::max(1, n);
+}
+
+template <int L2>
+void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    constexpr size_t SM = PassAShape<L2>::SMEM;
+    PassAParams p{};
+    p.n = (long long)pl.n;
+    p.log_n1 = pl.bk.log_n1;
+    p.log_n2 = pl.bk.log_n2;
+    p.r0 = r0;
+    p.r1 = r1;
+    p.ds = pl.bk.ds.as<double>();
+    p.skey = pl.bk.skey.as<unsigned>();
+    p.perm = pl.bk.perm.as<int>();
+    p.rowoff = pl.bk.rowoff.as<int>();
+    for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
+    auto fn = pl.uniform ? k1_passA<L2, true> : k1_passA<L2, false>;
+    set_smem(fn, SM);
+    const long long n1 = 1ll << pl.bk.log_n1;
+    const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, L2 / 16, SM));
+    fn<<<grid, L2 / 16, SM, s>>>(g, Z, p);
+    NB_LAUNCH();
+}
+
+template <int L1>
+void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    constexpr size_t SM = sizeof(double2) * (2 * padded_len(L1) + 16 + FftShapeX<L1>::TW_LEN);
+    PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+    auto fn = pl.uniform ? k1_passB<L1, true> : k1_passB<L1, false>;
+    set_smem(fn, SM);
+    const long long n2 = 1ll << pl.bk.log_n2;
+    const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
+    fn<<<grid, L1 / 16, SM, s>>>(Z, f, p);
+    NB_LAUNCH();
+}
+
+void dispatch_passA(int L, const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+    switch (L) {
+        case 16: return launch_passA<16>(g, Z, pl, r0, r1, s);
+        case 32: return launch_passA<32>(g, Z, pl, r0, r1, s);
+        case 64: return launch_passA<64>(g, Z, pl, r0, r1, s);
+        case 128: return launch_passA<128>(g, Z, pl, r0, r1, s);
+        case 256: return launch_passA<256>(g, Z, pl, r0, r1, s);
+        case 512: return launch_passA<512>(g, Z, pl, r0, r1, s);
+        case 1024: return launch_passA<1024>(g, Z, pl, r0, r1, s);
+        case 2048: return launch_passA<2048>(g, Z, pl, r0, r1, s);
+        case 4096: return launch_passA<4096>(g, Z, pl, r0, r1, s);
+        default: throw Error(kInternal, "pass A size");
+    }
+}
+
+void dispatch_passB(int L, const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+    switch (L) {
+        case 16: return launch_passB<16>(Z, f, pl, r0, r1, s);
+        case 32: return launch_passB<32>(Z, f, pl, r0, r1, s);
+        case 64: return launch_passB<64>(Z, f, pl, r0, r1, s);
+        case 128: return launch_passB<128>(Z, f, pl, r0, r1, s);
+        case 256: return launch_passB<256>(Z, f, pl, r0, r1, s);
+        case 512: return launch_passB<512>(Z, f, pl, r0, r1, s);
+        case 1024: return launch_passB<1024>(Z, f, pl, r0, r1, s);
+        case 2048: return launch_passB<2048>(Z, f, pl, r0, r1, s);
+        case 4096: return launch_passB<4096>(Z, f, pl, r0, r1, s);
+        default: throw Error(kInternal, "pass B size");
+    }
+}
+
+}  // namespace
+
+void exec_transpose_fused(const CorePlan& pl, const double2* g, double2* f, size_t batch,
+                          cudaStream_t s, cudaEvent_t* ev) {
+    ensure_bessel_constants(pl.device);
+    const size_t N = pl.n;
+    const int r0 = 0, r1 = (int)pl.K;
+    DevBuf Z(sizeof(double2) * N * (size_t)(r1 - r0), s);
+    const int L1 = 1 << pl.bk.log_n1, L2 = 1 << pl.bk.log_n2;
+    for (size_t b = 0; b < batch; ++b) {
+        if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[0], s));
+        dispatch_passA(L2, g + b * N, Z.as<double2>(), pl, r0, r1, s);
+        if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[1], s));
+        if (pl.bk.log_n1 == 0) {
+            k1_combine<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(Z.as<double2>(), f + b * N, (long long)N,
+                                                                 r0, r1, pl.uniform ? 1 : 0);
+            NB_LAUNCH();
+        } else {
+            dispatch_passB(L1, Z.as<double2>(), f + b * N, pl, r0, r1, s);
+        }
+        if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[2], s));
+    }
+}
+
+}  // namespace nb

@@ -1,0 +1,195 @@
+#!/usr/bin/env python3
+"""Per-configuration timing of every transform on the path.
+
+  python scripts/bench_configs.py [--steps K] [--warmup W] [--only cfg2,cfg3,...] [--out FILE]
+
+Times the device-pointer exec (inputs resident in HBM, plan built outside the
+timed region) with CUDA events on the launching stream, W warm-ups then K
+timed execs, and reports points/s, algorithmic bytes (the §8(d) formulas) and
+the HBM roofline fraction against MEASURED_PEAKS.json.  Also times the cuFFT
+comparison the reference's `bench` subcommand reports (fft_seconds_baseline:
+K batched Z2Z FFTs of size N, here through torch.fft = cuFFT) and the
+exec/FFT ratio (proj/tools/nufft_app.hpp:289-315 columns).  One JSON line per
+config; these are parity configurations, not bench.py's headline line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def timeit(fn, steps, warmup, stream):
+    import torch
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def cufft_ms(n, K, steps, warmup, stream):
+    import torch
+    x = torch.randn(n, dtype=torch.complex128, device="cuda")
+
+    def fn():
+        for _ in range(K):
+            torch.fft.fft(x)
+    return timeit(fn, steps, warmup, stream)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--only", default="cfg1,cfg2,cfg2adj,cfg3,cfg4,cfg5")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+
+    import paper_1701_04492_b200 as nb
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    P = peak()
+    rng = np.random.default_rng(7)
+    out = []
+    want = set(args.only.split(","))
+
+    def emit(name, desc, n_pts, ms, bytes_alg, K, plan_s, extra=None):
+        gbs = bytes_alg / (ms / 1e3) / 1e9 if bytes_alg else None
+        rec = {"config": name, "workload": desc, "points": n_pts, "ms_per_exec": ms,
+               "points_per_s": n_pts / (ms / 1e3), "rank_terms": K, "plan_seconds": plan_s,
+               "algorithmic_bytes": bytes_alg, "achieved_gbs": gbs,
+               "hbm_frac": (gbs / P) if gbs else None, "peak_gbs": P}
+        if extra:
+            rec.update(extra)
+        print(json.dumps(rec), flush=True)
+        out.append(rec)
+
+    def dev(a):
+        return torch.from_numpy(a).to("cuda")
+
+    if "cfg1" in want:
+        n = 1024
+        x = (np.arange(n) + rng.uniform(-0.5, 0.5, n)) / n
+        x = np.mod(x, 1.0)
+        t0 = time.perf_counter()
+        p = nb.plan_nufft2(x, 1e-14)
+        ps = time.perf_counter() - t0
+        c = dev(rng.standard_normal(n) + 1j * rng.standard_normal(n))
+        f = torch.empty_like(c)
+        ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), 200, 20, stream)
+        emit("cfg1", "NUFFT-II N=1024 eps=1e-14 jittered grid (latency)", n, ms, 44 * n, p.rank(), ps)
+
+    if "cfg2" in want or "cfg2adj" in want:
+        n = 1 << 24
+        x = rng.random(n)
+        t0 = time.perf_counter()
+        p = nb.plan_nufft2(x, 1e-14)
+        torch.cuda.synchronize()
+        ps = time.perf_counter() - t0
+        K = p.rank()
+        c = torch.randn(n, dtype=torch.complex128, device="cuda")
+        f = torch.empty_like(c)
+        cu = cufft_ms(n, K, args.steps, args.warmup, stream)
+        if "cfg2" in want:
+            ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), args.steps,
+                        args.warmup, stream)
+            emit("cfg2", "NUFFT-II N=2^24 eps=1e-14 x iid U[0,1)", n, ms, (32 + 12 + 32 * K) * n, K, ps,
+                 {"cufft_K_ffts_ms": cu, "exec_over_fft_ratio": ms / cu})
+        if "cfg2adj" in want:
+            lib = nb.lib()
+
+            def adj():
+                nb.api._check(lib.nufft_plan2_adjoint(p._h, f.data_ptr(), c.data_ptr(), sh))
+            try:
+                ms = timeit(adj, args.steps, args.warmup, stream)
+                emit("cfg2adj", "NUFFT-II adjoint (type-I core) N=2^24 eps=1e-14", n, ms,
+                     (32 + 12 + 32 * K) * n, K, ps, {"cufft_K_ffts_ms": cu, "exec_over_fft_ratio": ms / cu})
+            except Exception as exc:
+                print(json.dumps({"config": "cfg2adj", "error": str(exc)[:200]}), flush=True)
+        del p, c, f
+        torch.cuda.empty_cache()
+
+    if "cfg3" in want:
+        n = 1 << 24
+        w = np.clip(np.arange(n) + rng.uniform(-0.5, 0.5, n), 0, n)
+        t0 = time.perf_counter()
+        p = nb.plan_nufft1(w, 1e-14)
+        torch.cuda.synchronize()
+        ps = time.perf_counter() - t0
+        K = p.rank()
+        c = torch.randn(n, dtype=torch.complex128, device="cuda")
+        f = torch.empty_like(c)
+        ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), args.steps, args.warmup, stream)
+        cu = cufft_ms(n, K, args.steps, args.warmup, stream)
+        emit("cfg3", "NUFFT-I N=2^24 eps=1e-14 jittered frequencies", n, ms, (32 + 12 + 32 * K) * n, K, ps,
+             {"cufft_K_ffts_ms": cu, "exec_over_fft_ratio": ms / cu})
+        del p, c, f
+        torch.cuda.empty_cache()
+
+    if "cfg4" in want:
+        n = 1 << 22
+        x = rng.random(n)
+        w = rng.uniform(0, n, n)
+        t0 = time.perf_counter()
+        p = nb.plan_nufft3(x, w, 1e-14)
+        torch.cuda.synchronize()
+        ps = time.perf_counter() - t0
+        terms = p.effective_rank() * p.rank_inner
+        c = torch.randn(n, dtype=torch.complex128, device="cuda")
+        f = torch.empty_like(c)
+        ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), max(2, args.steps // 3),
+                    1, stream)
+        emit("cfg4", "NUFFT-III N=2^22 eps=1e-14 x U[0,1), omega U[0,N)", n, ms, (32 + 12 + 32 * terms) * n,
+             terms, ps, {"bTrivial": p.bTrivial, "effective_rank": p.effective_rank(), "rank_inner": p.rank_inner})
+        del p, c, f
+        torch.cuda.empty_cache()
+
+    if "cfg5" in want:
+        m = nn = 4096
+        cnt = 1 << 24
+        x, y = rng.random(cnt), rng.random(cnt)
+        t0 = time.perf_counter()
+        p = nb.plan_nufft2d2(x, y, m, nn, 1e-14)
+        torch.cuda.synchronize()
+        ps = time.perf_counter() - t0
+        k1, k2 = p.rank_x(), p.rank_y()
+        C2 = torch.randn(m, nn, dtype=torch.complex128, device="cuda")
+        f = torch.empty(cnt, dtype=torch.complex128, device="cuda")
+        ms = timeit(lambda: p.execute_device(C2.data_ptr(), f.data_ptr(), 1, sh), max(2, args.steps // 3),
+                    1, stream)
+        mn = m * nn
+        emit("cfg5", "2D NUFFT-II 4096x4096 -> 2^24 samples eps=1e-14", cnt, ms,
+             16 * mn + 32 * k1 * mn + 36 * cnt, k1 * k2, ps, {"rank_x": k1, "rank_y": k2,
+                                                              "fft_batches_of_2^24": k1 + k1 * k2})
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump(out, fh, indent=1)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -126,3 +126,19 @@ def test_cfg3_direct_sum_spot_check(nb):
     for j in np.random.default_rng(4).choice(N24, 6, replace=False):
         err = abs(f[j] - direct_type1_at(int(j), w, c))
         assert err <= 1e-12 * rms, (j, err, rms)
+
+
+def test_cfg2_adjoint_identity(nb, cfg2):
+    """<A c, g> == <c, A^H g> at full size (the fused transpose core against the
+    fused type-II passes), and the adjoint is bit-reproducible."""
+    x, c = cfg2
+    p = nb.plan_nufft2(x, 1e-14)
+    g = np.random.default_rng(5).standard_normal(N24) + 1j * np.random.default_rng(6).standard_normal(N24)
+    f = nb.exec_nufft2(p, c)
+    a1 = nb.exec_nufft2_adjoint(p, g)
+    a2 = nb.exec_nufft2_adjoint(p, g)
+    assert np.array_equal(a1.view(np.float64), a2.view(np.float64))
+    lhs = np.vdot(g, f)          # <A c, g> = g^H A c
+    rhs = np.vdot(a1, c)         # <c, A^H g> = (A^H g)^H c
+    scale = np.linalg.norm(g) * np.linalg.norm(f)
+    assert abs(lhs - rhs) <= 1e-13 * scale, (lhs, rhs)

@@ -150,6 +150,28 @@ def test_type1_vs_oracle(nb, port, n, eps):
     check(nb.exec_nufft1(pg, c), po.execute(c), eps)
 
 
+def test_type1_clustered_rows_overflow(nb, port):
+    """Frequencies packed into a few bins: fused pass-A rows far above the
+    per-CTA sample capacity (chunked accumulation) and long duplicate-bin runs."""
+    n = 1 << 14
+    rng = port.sampler(77)
+    w = 100.0 + rng.uniform_vector(n, 0.0, 6.0)
+    c = rng.complex_vector(n)
+    po, pg = port.plan1(w, 1e-12), nb.plan_nufft1(w, 1e-12)
+    check(nb.exec_nufft1(pg, c), po.execute(c), 1e-12)
+
+
+@pytest.mark.parametrize("n", [1 << 16, 1 << 17])
+def test_type1_fused_sizes_vs_oracle(nb, port, n):
+    """N1 < N2 and N1 == N2 splits of the fused transpose core."""
+    rng = port.sampler(400 + n)
+    w = rng.uniform_vector(n, 0.0, float(n))
+    c = rng.complex_vector(n)
+    po, pg = port.plan1(w, 1e-14), nb.plan_nufft1(w, 1e-14)
+    assert pg.fused
+    check(nb.exec_nufft1(pg, c), po.execute(c), 1e-14)
+
+
 @pytest.mark.parametrize("n", [16, 48, 256, 1024])
 def test_type3_vs_oracle(nb, port, n):
     for seed in range(3):
@@ -175,7 +197,7 @@ def test_type2d_vs_oracle(nb, port, m, n, cnt):
 
 
 def test_adjoint_vs_oracle(nb, port):
-    for n in (8, 32, 1000, 4096):
+    for n in (8, 16, 32, 128, 1000, 4096, 1 << 15):
         rng = port.sampler(30 + n)
         x = rng.uniform_vector(n, 0.0, 1.0)
         f = rng.complex_vector(n)
