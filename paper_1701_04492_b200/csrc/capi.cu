@@ -692,6 +692,7 @@ int nufft_plan2d2_create(const double* x_raw, const double* y_raw, size_t count_
                                                       (long long)st.count, (long long)m,
                                                       st.flat.as<long long>());
         NB_LAUNCH();
+        if (nb::fused_2d_eligible(m, n, st.count)) nb::build_2d_fused(st, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });
@@ -717,6 +718,7 @@ int nufft_plan2d2_info(const nufft_plan2d* plan, nufft_plan_info* info) {
         info->m = st.m;
         info->ncols = st.n;
         info->device = st.device;
+        info->path = st.fused ? 1 : 0;
     });
 }
 int nufft_plan2d2_samples(const nufft_plan2d* plan, double* x, double* y, long* sx, long* sy,

@@ -55,6 +55,14 @@ __global__ void k2d_accum(const double2* __restrict__ fullT, double2* __restrict
 
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s) {
+    if (p.fused) {
+        exec_2d_fused(p, C, f, batch, s);
+        for (size_t b = 0; b < batch; ++b) {  // logical transform counts as the reference
+            fft_count(p.n, p.m * p.kx * (reuse_rows ? 1 : p.ky));
+            fft_count(p.m, p.n * p.kx * p.ky);
+        }
+        return;
+    }
     ensure_bessel_constants(p.device);
     const size_t m = p.m, n = p.n, mn = m * n, count = p.count;
     DevBuf rs(sizeof(double2) * mn, s), rsT(sizeof(double2) * mn, s), full(sizeof(double2) * mn, s);

@@ -1,0 +1,408 @@
+// Fused 2D type-II execution (power-of-two grids, 16 <= m, n <= 4096).
+//
+// Reference: exec_nufft2d2_impl transform2d.hpp:107-147
+//   f_j = sum_{r1<Kx} sum_{r2<Ky} ux_r1[j] uy_r2[j] [F_m D_vy_r2 C D_vx_r1 F_n^T](ty_j, tx_j)
+// evaluated by the reference as Kx row stages (m FFTs of size n, reused over
+// r2) and Kx*Ky column stages (n FFTs of size m), each followed by a gather
+// over all samples.  Here:
+//
+//  row kernel (CTA per row ky, persistent): the C row is read once into
+//    shared memory; for every r1 it is scaled by vx_r1(kx) (Chebyshev state in
+//    registers), transformed (n-point FFT) and R_r1[ky][tx] is written
+//    (row-major, full sectors) — the only HBM round trip of the row stage.
+//  column kernel (CTA per column tx, persistent): the samples with tx_j = tx
+//    (plan-time stable sort) stay in shared memory/registers for all Kx*Ky
+//    terms.  For r1 = Kx-1..0 the column R_r1[:][tx] is staged in shared
+//    memory once; for r2 = Ky-1..0 the column is scaled by vy_r2 (a Ky x m
+//    table, L2-resident), transformed (m-point FFT) and every sample updates
+//        S_j <- S_j (i hy_j) + gy_r2(hy_j^2) X[ty_j]              (Horner in r2),
+//    then A_j <- A_j (i hx_j) + gx_r1(hx_j^2) S_j                 (Horner in r1,
+//    A_j in an HBM scratch in sorted order, coalesced), and finally
+//    f_j = 4 exp(2i(hx_j + hy_j)) A_j — the Bessel form of the reference's
+//    ux*uy (bessel.cuh) without materializing either factor.
+//
+// HBM bytes: C 16 mn + R 32 Kx mn + A 32 Kx count + f 16 count + sample data;
+// the Kx*Ky column FFTs never leave the SM.
+#include <algorithm>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "bessel.cuh"
+#include "fft_block.cuh"
+#include "plans.hpp"
+
+namespace nb {
+
+namespace {
+
+inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+constexpr int kQ2d = 20;  // samples per column-kernel thread (capacity 1.25 m per chunk)
+
+struct RowParams {
+    long long m, n;
+    int log_n;
+    int kx;
+    int ux_uniform;
+};
+
+struct ColParams {
+    long long m, n;
+    int log_n;
+    int kx, ky;
+    int ux_uniform, uy_uniform;
+    const double* dxs;
+    const double* dys;
+    const unsigned short* tys;
+    const int* perm;
+    const int* coloff;
+    const double* vyt;  // ky x m
+    double2* A;         // sorted-order scratch
+    int degx[kRankCap];
+    int degy[kRankCap];
+};
+
+// ---------------------------------------------------------------- row stage
+template <int LN>
+__global__ void __launch_bounds__(LN / 16, 1)
+    k2d_rows(const double2* __restrict__ C, double2* __restrict__ R, RowParams p) {
+    constexpr int G = LN / 16;
+    extern __shared__ double2 smem[];
+    double2* crow = smem;
+    double2* buf0 = crow + LN;
+    double2* buf1 = buf0 + padded_len(LN);
+    double2* tw = buf1 + padded_len(LN);
+    const int tid = threadIdx.x;
+    twiddle_table_build<LN>(tw, tid, G);
+    Twiddles<LN> T;
+    twiddle_init<LN>(T, tw, tid);
+    const long long mn = p.m * p.n;
+    // 2 s_q = 4 kx / n - 2 with kx = tid + q G  ->  two_s0 + q/4 (exact)
+    const double two_s0 = (double)(4 * tid) / (double)p.n - 2.0;
+    for (long long ky = blockIdx.x; ky < p.m; ky += gridDim.x) {
+        __syncthreads();  // previous row's readers of crow are done
+#pragma unroll
+        for (int q = 0; q < 16; ++q) crow[tid + q * G] = __ldcs(C + ky * p.n + tid + q * G);
+        double tcur[16], tprev[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            tprev[q] = 1.0;
+            tcur[q] = 0.5 * (two_s0 + 0.25 * q);
+        }
+        __syncthreads();
+        for (int r = 0; r < p.kx; ++r) {
+            if constexpr (FftShape<LN>::STAGES < 3) __syncthreads();
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 cv = crow[tid + q * G];
+                const double vr = p.ux_uniform ? 1.0 : ((r == 0) ? 0.5 : tcur[q]);
+                v[q] = make_double2(cv.x * vr, cv.y * vr);
+            }
+            block_fft<LN, -1>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
+            double2* out = R + (long long)r * mn + ky * p.n;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) out[tid + q * G] = v[q];
+            if (r > 0) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                    tprev[q] = tcur[q];
+                    tcur[q] = tn;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- column stage
+template <int LM>
+struct ColShape {
+    static constexpr int G = LM / 16;
+    static constexpr int CAP = kQ2d * G;
+    static constexpr size_t SMEM = sizeof(double2) * (LM + padded_len(LM) + FftShapeX<LM>::TW_LEN) +
+                                   (sizeof(double) + sizeof(unsigned short)) * CAP;
+    static_assert(SMEM <= 227 * 1024, "column kernel shared memory");
+};
+
+template <int LM>
+__global__ void __launch_bounds__(LM / 16, 1)
+    k2d_cols(const double2* __restrict__ R, double2* __restrict__ f, ColParams p) {
+    using S = ColShape<LM>;
+    constexpr int G = S::G;
+    constexpr int Q = kQ2d;
+    constexpr int CAP = S::CAP;
+    constexpr int CH = 4;  // Horner chunk (independent FMA chains per coefficient)
+    extern __shared__ double2 smem[];
+    double2* rcol = smem;
+    double2* buf = rcol + LM;  // FFT exchange; holds X between the FFT and the gathers
+    double2* tw = buf + padded_len(LM);
+    double* shy = reinterpret_cast<double*>(tw + FftShapeX<LM>::TW_LEN);
+    unsigned short* sty = reinterpret_cast<unsigned short*>(shy + CAP);
+    const int tid = threadIdx.x;
+    twiddle_table_build<LM>(tw, tid, G);
+    Twiddles<LM> T;
+    twiddle_init<LM>(T, tw, tid);
+    __syncthreads();
+    const long long mn = p.m * p.n;
+    for (long long tx = blockIdx.x; tx < p.n; tx += gridDim.x) {
+        const int beg = p.coloff[tx], end = p.coloff[tx + 1];
+        for (int cb = beg; cb < end; cb += CAP) {
+            const int cnt = min(CAP, end - cb);
+            __syncthreads();  // previous chunk's readers of shy / sty are done
+            for (int i = tid; i < CAP; i += G) {
+                const bool ok = i < cnt;
+                shy[i] = (ok && !p.uy_uniform) ? half_phase(p.dys[cb + i]) : 0.0;
+                sty[i] = ok ? p.tys[cb + i] : (unsigned short)0;
+            }
+            for (int r1 = p.kx - 1; r1 >= 0; --r1) {
+                __syncthreads();  // previous term's gathers from buf / reads of rcol done
+                const double2* col = R + (long long)r1 * mn + tx;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) rcol[tid + q * G] = __ldcs(col + (long long)(tid + q * G) * p.n);
+                double2 acc[Q];
+#pragma unroll
+                for (int u = 0; u < Q; ++u) acc[u] = make_double2(0.0, 0.0);
+                for (int r2 = p.ky - 1; r2 >= 0; --r2) {
+                    double2 v[16];
+                    const double* vy = p.vyt + (long long)r2 * p.m;
+                    __syncthreads();  // rcol visible; previous gathers from buf done
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
+                    block_fft_1buf<LM, -1>(v, buf, tid, T, [] { __syncthreads(); });
+                    __syncthreads();  // last-stage reads of buf done
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    __syncthreads();
+                    // S <- S (i hy) + gy_r2(hy^2) X[ty]
+                    const double* a = kBes + r2 * kSeriesTerms;
+                    const int deg = p.degy[r2];
+#pragma unroll
+                    for (int u0 = 0; u0 < Q; u0 += CH) {
+                        double h[CH], w[CH], g[CH];
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            h[c] = shy[tid + (u0 + c) * G];
+                            w[c] = h[c] * h[c];
+                            g[c] = 0.0;
+                        }
+                        if (p.uy_uniform) {
+#pragma unroll
+                            for (int c = 0; c < CH; ++c) g[c] = 1.0;
+                        } else {
+                            for (int m = deg; m >= 0; --m) {
+                                const double am = a[m];
+#pragma unroll
+                                for (int c = 0; c < CH; ++c) g[c] = __fma_rn(g[c], w[c], am);
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) {
+                            const int u = u0 + c;
+                            const double2 X = buf[sty[tid + u * G]];
+                            const double ax = acc[u].x;
+                            acc[u].x = __fma_rn(g[c], X.x, -h[c] * acc[u].y);
+                            acc[u].y = __fma_rn(g[c], X.y, h[c] * ax);
+                        }
+                    }
+                }
+                // A <- A (i hx) + gx_r1(hx^2) S ; the last term writes f
+                const double* a = kBes + r1 * kSeriesTerms;
+                const int deg = p.degx[r1];
+#pragma unroll
+                for (int u = 0; u < Q; ++u) {
+                    const int i = tid + u * G;
+                    if (i >= cnt) continue;
+                    const double hx = p.ux_uniform ? 0.0 : half_phase(p.dxs[cb + i]);
+                    double gx = 1.0;
+                    if (!p.ux_uniform) {
+                        const double w = hx * hx;
+                        gx = 0.0;
+                        for (int m = deg; m >= 0; --m) gx = __fma_rn(gx, w, a[m]);
+                    }
+                    double2 A = cscale(acc[u], gx);
+                    if (r1 != p.kx - 1) {
+                        const double2 prev = p.A[cb + i];
+                        A.x = __fma_rn(-hx, prev.y, A.x);
+                        A.y = __fma_rn(hx, prev.x, A.y);
+                    }
+                    if (r1 > 0) {
+                        p.A[cb + i] = A;
+                    } else {
+                        double ph = 0.0, scale = 1.0;
+                        if (!p.ux_uniform) {
+                            ph += 2.0 * hx;
+                            scale *= 2.0;
+                        }
+                        if (!p.uy_uniform) {
+                            ph += 2.0 * shy[i];
+                            scale *= 2.0;
+                        }
+                        double sn = 0.0, cs = 1.0;
+                        if (ph != 0.0) sincos(ph, &sn, &cs);
+                        __stcs(f + p.perm[cb + i], cmul(make_double2(scale * cs, scale * sn), A));
+                    }
+                }
+            }
+        }
+    }
+}
+
+__global__ void k2d_keys(const long long* __restrict__ tx, long long count, unsigned* __restrict__ keys,
+                         int* __restrict__ idx) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= count) return;
+    keys[j] = (unsigned)tx[j];
+    idx[j] = (int)j;
+}
+
+__global__ void k2d_offsets(const unsigned* __restrict__ keys, long long count, long long nb,
+                            int* __restrict__ off) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i > count) return;
+    const long long cur = (i < count) ? (long long)keys[i] : nb;
+    const long long prev = (i > 0) ? (long long)keys[i - 1] : -1;
+    for (long long b = prev + 1; b <= cur; ++b) off[b] = (int)i;
+}
+
+__global__ void k2d_gather(const int* __restrict__ perm, long long count, const double* __restrict__ dx,
+                           const double* __restrict__ dy, const long long* __restrict__ ty,
+                           double* __restrict__ dxs, double* __restrict__ dys,
+                           unsigned short* __restrict__ tys) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int j = perm[i];
+    dxs[i] = dx[j];
+    dys[i] = dy[j];
+    tys[i] = (unsigned short)ty[j];
+}
+
+__global__ void k2d_vtable(double* __restrict__ vt, long long m, int K, int uniform) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m * K) return;
+    const int r = (int)(i / m);
+    const long long k = i % m;
+    vt[i] = uniform ? 1.0 : v_factor_from_s(grid_s(k, m), r);
+}
+
+template <class F>
+void set_smem(F* fn, size_t bytes) {
+    NB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+int occupancy(const void* fn, int threads, size_t smem) {
+    int n = 0;
+    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    return std::max(1, n);
+}
+
+template <int LN>
+void launch_rows(const double2* C, double2* R, const Plan2DState& st, cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(st.device);
+    constexpr size_t SM = sizeof(double2) * (LN + 2 * padded_len(LN) + FftShapeX<LN>::TW_LEN);
+    RowParams p{(long long)st.m, (long long)st.n, ilog2(st.n), (int)st.kx, st.ux_uniform ? 1 : 0};
+    set_smem(k2d_rows<LN>, SM);
+    const int grid = (int)std::min<long long>((long long)st.m,
+                                              (long long)ctx.sms * occupancy((const void*)k2d_rows<LN>, LN / 16, SM));
+    k2d_rows<LN><<<grid, LN / 16, SM, s>>>(C, R, p);
+    NB_LAUNCH();
+}
+
+template <int LM>
+void launch_cols(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(st.device);
+    constexpr size_t SM = ColShape<LM>::SMEM;
+    ColParams p{};
+    p.m = (long long)st.m;
+    p.n = (long long)st.n;
+    p.log_n = ilog2(st.n);
+    p.kx = (int)st.kx;
+    p.ky = (int)st.ky;
+    p.ux_uniform = st.ux_uniform ? 1 : 0;
+    p.uy_uniform = st.uy_uniform ? 1 : 0;
+    p.dxs = st.fz.dxs.as<double>();
+    p.dys = st.fz.dys.as<double>();
+    p.tys = st.fz.tys.as<unsigned short>();
+    p.perm = st.fz.perm.as<int>();
+    p.coloff = st.fz.coloff.as<int>();
+    p.vyt = st.fz.vyt.as<double>();
+    p.A = A;
+    for (size_t r = 0; r < st.deg_x.size() && r < (size_t)kRankCap; ++r) p.degx[r] = st.deg_x[r];
+    for (size_t r = 0; r < st.deg_y.size() && r < (size_t)kRankCap; ++r) p.degy[r] = st.deg_y[r];
+    set_smem(k2d_cols<LM>, SM);
+    const int grid = (int)std::min<long long>((long long)st.n,
+                                              (long long)ctx.sms * occupancy((const void*)k2d_cols<LM>, LM / 16, SM));
+    k2d_cols<LM><<<grid, LM / 16, SM, s>>>(R, f, p);
+    NB_LAUNCH();
+}
+
+#define NB_SIZE_SWITCH(L, CALL)                 \
+    switch (L) {                                \
+        case 16: { constexpr int LL = 16; CALL; break; }     \
+        case 32: { constexpr int LL = 32; CALL; break; }     \
+        case 64: { constexpr int LL = 64; CALL; break; }     \
+        case 128: { constexpr int LL = 128; CALL; break; }   \
+        case 256: { constexpr int LL = 256; CALL; break; }   \
+        case 512: { constexpr int LL = 512; CALL; break; }   \
+        case 1024: { constexpr int LL = 1024; CALL; break; } \
+        case 2048: { constexpr int LL = 2048; CALL; break; } \
+        case 4096: { constexpr int LL = 4096; CALL; break; } \
+        default: throw Error(kInternal, "2D fused size");    \
+    }
+
+}  // namespace
+
+bool fused_2d_eligible(size_t m, size_t n, size_t count) {
+    if (!is_pow2(m) || !is_pow2(n) || m < 16 || n < 16 || m > 4096 || n > 4096) return false;
+    // the column kernel re-runs all terms per chunk of kQ2d*m/16 samples of a
+    // column: take it only while the average column fits about one chunk
+    const double per_col = (double)count / (double)n;
+    return per_col <= 1.1 * (double)(kQ2d * (m / 16)) && count < (size_t(1) << 31);
+}
+
+void build_2d_fused(Plan2DState& st, cudaStream_t s) {
+    const size_t count = st.count, n = st.n, m = st.m;
+    DevBuf keys(4 * count, s), keys_out(4 * count, s), idx(4 * count, s);
+    st.fz.perm.alloc(4 * count);
+    k2d_keys<<<blocks(count), 256, 0, s>>>(st.ax.t.as<long long>(), (long long)count, keys.as<unsigned>(),
+                                          idx.as<int>());
+    NB_LAUNCH();
+    const int bits = std::max(1, ilog2(n));
+    size_t temp = 0;
+    NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
+                                            idx.as<int>(), st.fz.perm.as<int>(), (int)count, 0, bits, s));
+    DevBuf tb(temp, s);
+    NB_CUDA(cub::DeviceRadixSort::SortPairs(tb.get(), temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
+                                            idx.as<int>(), st.fz.perm.as<int>(), (int)count, 0, bits, s));
+    st.fz.coloff.alloc(4 * (n + 1));
+    k2d_offsets<<<blocks(count + 1), 256, 0, s>>>(keys_out.as<unsigned>(), (long long)count, (long long)n,
+                                                 st.fz.coloff.as<int>());
+    NB_LAUNCH();
+    st.fz.dxs.alloc(8 * count);
+    st.fz.dys.alloc(8 * count);
+    st.fz.tys.alloc(2 * count);
+    k2d_gather<<<blocks(count), 256, 0, s>>>(st.fz.perm.as<int>(), (long long)count, st.ax.delta.as<double>(),
+                                            st.ay.delta.as<double>(), st.ay.t.as<long long>(),
+                                            st.fz.dxs.as<double>(), st.fz.dys.as<double>(),
+                                            st.fz.tys.as<unsigned short>());
+    NB_LAUNCH();
+    st.fz.vyt.alloc(8 * m * st.ky);
+    k2d_vtable<<<blocks(m * st.ky), 256, 0, s>>>(st.fz.vyt.as<double>(), (long long)m, (int)st.ky,
+                                                st.uy_uniform ? 1 : 0);
+    NB_LAUNCH();
+    st.fused = true;
+}
+
+void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s) {
+    ensure_bessel_constants(st.device);
+    const size_t mn = st.m * st.n;
+    DevBuf R(sizeof(double2) * mn * st.kx, s);
+    DevBuf A(sizeof(double2) * std::max<size_t>(st.count, 1), s);
+    const int LN = (int)st.n, LM = (int)st.m;
+    for (size_t b = 0; b < batch; ++b) {
+        NB_SIZE_SWITCH(LN, launch_rows<LL>(C + b * mn, R.as<double2>(), st, s));
+        NB_SIZE_SWITCH(LM, launch_cols<LL>(R.as<double2>(), f + b * st.count, A.as<double2>(), st, s));
+    }
+}
+
+}  // namespace nb

@@ -75,6 +75,13 @@ struct Plan2DState {
     bool ux_uniform = true, uy_uniform = true;
     std::vector<int> deg_x, deg_y;
     DevArray flat;               // m*tx + ty (int64)
+    // fused path (nufft2d_fused.cu): samples sorted by column tx (stable)
+    bool fused = false;
+    struct {
+        DevArray perm, coloff;   // int32 original index, n+1 column offsets
+        DevArray dxs, dys, tys;  // sorted delta_x, delta_y (fp64), ty (uint16)
+        DevArray vyt;            // vy_r2(ky) table, ky x m (fp64)
+    } fz;
 };
 
 // ---- plan construction (plan_kernels.cu) --------------------------------
@@ -109,6 +116,10 @@ void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_
 void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s);
+
+bool fused_2d_eligible(size_t m, size_t n, size_t count);
+void build_2d_fused(Plan2DState& st, cudaStream_t s);
+void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s);
 
 // elementwise helpers shared by the generic paths (generic_kernels.cu)
 void conj_copy(const double2* in, double2* out, size_t n, cudaStream_t s);

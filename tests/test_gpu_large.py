@@ -142,3 +142,30 @@ def test_cfg2_adjoint_identity(nb, cfg2):
     rhs = np.vdot(a1, c)         # <c, A^H g> = (A^H g)^H c
     scale = np.linalg.norm(g) * np.linalg.norm(f)
     assert abs(lhs - rhs) <= 1e-13 * scale, (lhs, rhs)
+
+
+def _exact_frac_phase(x: float, k: np.ndarray) -> np.ndarray:
+    """frac(x * k) for integer k < 2^24 with the product reduced exactly."""
+    m = int(round(x * 2 ** 29))
+    lo = x - m / 2 ** 29
+    return ((m * k) & ((1 << 29) - 1)).astype(np.float64) / 2 ** 29 + lo * k.astype(np.float64)
+
+
+def test_cfg5_direct_sum_spot_check(nb):
+    """2D 4096 x 4096 -> 2^24 samples, eps 1e-14 (cfg5) against exact direct sums."""
+    m = n = 4096
+    cnt = 1 << 24
+    rng = np.random.default_rng(55)
+    x, y = rng.random(cnt), rng.random(cnt)
+    C2 = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    p = nb.plan_nufft2d2(x, y, m, n, 1e-14)
+    assert p.fused
+    f = nb.exec_nufft2d2(p, C2)
+    rms = np.sqrt(np.mean(np.abs(f) ** 2))
+    kx = np.arange(n, dtype=np.int64)
+    ky = np.arange(m, dtype=np.int64)
+    for j in np.random.default_rng(9).choice(cnt, 4, replace=False):
+        ex = np.exp(-2j * np.pi * _exact_frac_phase(float(x[j]), kx))
+        ey = np.exp(-2j * np.pi * _exact_frac_phase(float(y[j]), ky))
+        want = complex(ey @ (C2 @ ex))
+        assert abs(f[j] - want) <= 1e-13 * rms, (j, abs(f[j] - want), rms)

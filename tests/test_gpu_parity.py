@@ -196,6 +196,34 @@ def test_type2d_vs_oracle(nb, port, m, n, cnt):
     check(nb.exec_nufft2d2(pg, C2), po.execute(C2), 1e-9)
 
 
+@pytest.mark.parametrize("m,n,cnt", [(16, 16, 300), (256, 128, 20000), (128, 512, 40000)])
+def test_type2d_fused_vs_oracle(nb, port, m, n, cnt):
+    """Power-of-two grids take the fused row/column kernels."""
+    rng = port.sampler(900 + m + n)
+    x = rng.uniform_vector(cnt, 0.0, 1.0)
+    y = rng.uniform_vector(cnt, 0.0, 1.0)
+    C2 = rng.complex_vector(m * n).reshape(m, n)
+    po, pg = port.plan2d2(x, y, m, n, 1e-12), nb.plan_nufft2d2(x, y, m, n, 1e-12)
+    assert pg.fused
+    check(nb.exec_nufft2d2(pg, C2), po.execute(C2), 1e-12)
+    check(nb.exec_nufft2d2_impl(pg, C2, False), po.execute(C2), 1e-12)
+
+
+def test_type2d_fused_clustered_and_uniform_axes(nb, port):
+    """Columns far above the per-CTA capacity (chunked), and on-grid axes
+    (u = v = 1 on that axis)."""
+    m, n = 64, 32
+    rng = port.sampler(4242)
+    cnt = 1500
+    x = (0.25 + rng.uniform_vector(cnt, 0.0, 1.0) * 2.0 / n) % 1.0     # ~2 columns
+    y = rng.uniform_vector(cnt, 0.0, 1.0)
+    C2 = rng.complex_vector(m * n).reshape(m, n)
+    for xx, yy in ((x, y), (np.arange(cnt) % n / n, y), (x, np.arange(cnt) % m / m)):
+        po, pg = port.plan2d2(xx, yy, m, n, 1e-12), nb.plan_nufft2d2(xx, yy, m, n, 1e-12)
+        assert (pg.rank_x(), pg.rank_y()) == po.info2d()[:2]
+        check(nb.exec_nufft2d2(pg, C2), po.execute(C2), 1e-12)
+
+
 def test_adjoint_vs_oracle(nb, port):
     for n in (8, 16, 32, 128, 1000, 4096, 1 << 15):
         rng = port.sampler(30 + n)
