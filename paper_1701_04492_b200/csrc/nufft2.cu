@@ -31,6 +31,7 @@
 #include "bessel.cuh"
 #include "fft_block.cuh"
 #include "plans.hpp"
+#include "tmem.cuh"
 
 namespace nb {
 
@@ -145,6 +146,128 @@ __global__ void __launch_bounds__(L1 / 16, 1)
     }
 }
 
+// Two-group pass 1 (L1 = 2048, 4096): a CTA runs two independent column
+// workers of G threads each (columns 2*blockIdx + g, stride 2*gridDim), so
+// twice as many warps hide the exchange and store latencies.  What kept the
+// single-group kernel at one worker per SM — the cached c column (64 KB of
+// shared memory) and the Chebyshev state (64 registers per thread) — lives in
+// tensor memory instead (tmem.cuh): per thread 128 columns, [c re/im lo/hi x
+// 16 points][T_{r-1}, T_r lo/hi x 16 points], read and advanced 4 points at a
+// time.  Each worker exchanges through one padded buffer of its own.
+template <int L1>
+struct P1TmShape {
+    static constexpr int G = L1 / 16;
+    static constexpr int THREADS = 2 * G;
+    static constexpr size_t SMEM = sizeof(double2) * (2 * padded_len(L1) + 2 * 16 + FftShapeX<L1>::TW_LEN);
+    static_assert((THREADS / 32 + 3) / 4 * 128 <= 512, "TMEM columns");
+};
+
+template <int L1, bool UNIFORM>
+__global__ void __launch_bounds__(2 * (L1 / 16), 1)
+    k2_pass1_tm(const double2* __restrict__ c, double2* __restrict__ Y, Pass1Params p) {
+    constexpr int G = L1 / 16;
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x / G;
+    const int tid = threadIdx.x - grp * G;
+    double2* buf = smem + grp * padded_len(L1);
+    double2* step = smem + 2 * padded_len(L1) + grp * 16;
+    double2* tw = smem + 2 * padded_len(L1) + 32;
+    twiddle_table_build<L1>(tw, threadIdx.x, 2 * G);
+    Twiddles<L1> T;
+    twiddle_init<L1>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 128);
+    const unsigned tc_c = tcol, tc_s = tcol + 64;
+    const int bar = 1 + grp;
+    auto gsync = [bar] { nbar_sync(bar, G); };
+    const long long n2 = 1ll << p.log_n2;
+    const long long N = p.n;
+    for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
+        gsync();  // previous column's readers of step are done
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
+        const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
+        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+        // column of c and the Chebyshev state (T_{r0-1}, T_r0) into TMEM
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            unsigned cv[16], sv[16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = 4 * j + u;
+                const double2 x = __ldg(c + (((long long)(tid + q * G)) << p.log_n2) + k2);
+                cv[4 * u] = lo32(x.x);
+                cv[4 * u + 1] = hi32(x.x);
+                cv[4 * u + 2] = lo32(x.y);
+                cv[4 * u + 3] = hi32(x.y);
+                const double ts = two_s0 + 0.25 * q;
+                double tprev = 1.0, tcur = 0.5 * ts;
+                for (int r = 1; r < p.r0; ++r) {
+                    const double tn = __fma_rn(ts, tcur, -tprev);
+                    tprev = tcur;
+                    tcur = tn;
+                }
+                sv[4 * u] = lo32(tprev);
+                sv[4 * u + 1] = hi32(tprev);
+                sv[4 * u + 2] = lo32(tcur);
+                sv[4 * u + 3] = hi32(tcur);
+            }
+            tm_st16(tc_c + 16 * j, cv);
+            if constexpr (!UNIFORM) tm_st16(tc_s + 16 * j, sv);
+        }
+        tm_wait_st();
+        gsync();  // step visible
+        for (int r = p.r0; r < p.r1; ++r) {
+            double2 v[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                unsigned cv[16], sv[16];
+                tm_ld16(tc_c + 16 * j, cv);
+                if constexpr (!UNIFORM) tm_ld16(tc_s + 16 * j, sv);
+                tm_wait_ld();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = 4 * j + u;
+                    const double2 x = make_double2(mk64(cv[4 * u], cv[4 * u + 1]), mk64(cv[4 * u + 2], cv[4 * u + 3]));
+                    if constexpr (UNIFORM) {
+                        v[q] = x;
+                    } else {
+                        const double tprev = mk64(sv[4 * u], sv[4 * u + 1]);
+                        const double tcur = mk64(sv[4 * u + 2], sv[4 * u + 3]);
+                        const double vr = (r == 0) ? 0.5 : tcur;
+                        v[q] = make_double2(x.x * vr, x.y * vr);
+                        if (r > 0) {  // (T_{r-1}, T_r) -> (T_r, T_{r+1})
+                            const double tn = __fma_rn(two_s0 + 0.25 * q, tcur, -tprev);
+                            sv[4 * u] = sv[4 * u + 2];
+                            sv[4 * u + 1] = sv[4 * u + 3];
+                            sv[4 * u + 2] = lo32(tn);
+                            sv[4 * u + 3] = hi32(tn);
+                        }
+                    }
+                }
+                if constexpr (!UNIFORM) {
+                    if (r > 0) tm_st16(tc_s + 16 * j, sv);
+                }
+            }
+            gsync();  // previous term's last-stage reads of buf are done
+            block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 w = cmul(base, step[q]);
+                const long long t1 = tid + q * G;
+                Y[y_index(r - p.r0, N, p.log_n2, t1, k2)] = cmul(v[q], w);
+            }
+        }
+        tm_wait_st();
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
 // pass 1 for N1 == 1: Y_r[k] = v_r(k) c[k]
 __global__ void k2_scale(const double2* __restrict__ c, double2* __restrict__ Y, long long N,
                          int r0, int r1, int uniform) {
@@ -189,13 +312,50 @@ struct Pass2Params {
         if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[(slot)] = clock64();           \
     } while (0)
 
+// g_r(w) for C samples at once, degree D fixed at compile time: one
+// (uniform, constant-bank) coefficient load feeds C independent FMAs.
+template <int C, int D>
+__device__ __forceinline__ void series_fixed(double (&g)[C], const double (&w)[C], const double* a) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) g[c] = a[D];
+#pragma unroll
+    for (int m = D - 1; m >= 0; --m) {
+        const double am = a[m];
+#pragma unroll
+        for (int c = 0; c < C; ++c) g[c] = __fma_rn(g[c], w[c], am);
+    }
+}
+
+// runtime degree (warp-uniform) -> unrolled straight-line Horner
+template <int C>
+__device__ __forceinline__ void series_deg(double (&g)[C], const double (&w)[C], const double* a, int deg) {
+    switch (deg) {
+        case 0: series_fixed<C, 0>(g, w, a); break;
+        case 1: series_fixed<C, 1>(g, w, a); break;
+        case 2: series_fixed<C, 2>(g, w, a); break;
+        case 3: series_fixed<C, 3>(g, w, a); break;
+        case 4: series_fixed<C, 4>(g, w, a); break;
+        case 5: series_fixed<C, 5>(g, w, a); break;
+        case 6: series_fixed<C, 6>(g, w, a); break;
+        case 7: series_fixed<C, 7>(g, w, a); break;
+        case 8: series_fixed<C, 8>(g, w, a); break;
+        case 9: series_fixed<C, 9>(g, w, a); break;
+        case 10: series_fixed<C, 10>(g, w, a); break;
+        case 11: series_fixed<C, 11>(g, w, a); break;
+        case 12: series_fixed<C, 12>(g, w, a); break;
+        case 13: series_fixed<C, 13>(g, w, a); break;
+        case 14: series_fixed<C, 14>(g, w, a); break;
+        default: series_fixed<C, kSeriesTerms - 1>(g, w, a); break;
+    }
+}
+
 // One Horner step in r for the thread's samples: acc <- acc*(i h) + g_r(h^2) X_r[t2].
-// Samples go in chunks of C: the degree-`deg` series for g_r runs as one
-// runtime loop whose coefficient (uniform, constant bank) feeds C independent
-// FMAs; acc stays in registers (the chunk loop is unrolled).
+// Samples go in chunks of C with a straight-line series per chunk; slots past
+// the chunk's sample count hold h = 0, t2 = 0 (load_samples) so no lane
+// predication is needed (their accumulators are never stored).
 template <int Q, int G>
 __device__ __forceinline__ void horner_step(double2 (&acc)[Q], int r, int deg, const double2* xb,
-                                            const int* st2, const double* sh, int tid, int cnt) {
+                                            const int* st2, const double* sh, int tid) {
     constexpr int C = 4;
     const double* a = kBes + r * kSeriesTerms;
 #pragma unroll
@@ -203,22 +363,15 @@ __device__ __forceinline__ void horner_step(double2 (&acc)[Q], int r, int deg, c
         double h[C], w[C], g[C];
 #pragma unroll
         for (int u = 0; u < C; ++u) {
-            const int i = tid + (q0 + u) * G;
-            h[u] = (q0 + u < Q && i < cnt) ? sh[i] : 0.0;
+            h[u] = (q0 + u < Q) ? sh[tid + (q0 + u) * G] : 0.0;
             w[u] = h[u] * h[u];
-            g[u] = 0.0;
         }
-        for (int m = deg; m >= 0; --m) {
-            const double am = a[m];
-#pragma unroll
-            for (int u = 0; u < C; ++u) g[u] = __fma_rn(g[u], w[u], am);
-        }
+        series_deg<C>(g, w, a, deg);
 #pragma unroll
         for (int u = 0; u < C; ++u) {
             const int q = q0 + u;
-            const int i = tid + q * G;
-            if (q < Q && i < cnt) {
-                const double2 X = xb[st2[i]];
+            if (q < Q) {
+                const double2 X = xb[st2[tid + q * G]];
                 const double ax = acc[q].x;
                 acc[q].x = __fma_rn(g[u], X.x, -h[u] * acc[q].y);
                 acc[q].y = __fma_rn(g[u], X.y, h[u] * ax);
@@ -244,6 +397,9 @@ __device__ __forceinline__ void load_samples(const Pass2Params& p, int cb, int c
             const long long t = sj & (p.n - 1);
             st2[i] = (int)(t >> p.log_n1);
             sh[i] = half_phase(d);
+        } else {  // idle slot: harmless inputs for the unpredicated Horner step
+            st2[i] = 0;
+            sh[i] = 0.0;
         }
     }
 }
@@ -324,7 +480,7 @@ __global__ void __launch_bounds__(L2 / 16)
                         if (i < cnt) acc[q] = xb[st2[i]];
                     }
                 } else {
-                    horner_step<Q, G>(acc, r, p.deg[r], xb, st2, sh, tid, cnt);
+                    horner_step<Q, G>(acc, r, p.deg[r], xb, st2, sh, tid);
                 }
                 __syncthreads();
             }
@@ -472,7 +628,7 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
                             if (j < cnt) acc[q] = xb[st2[j]];
                         }
                     } else {
-                        horner_step<Q, S>(acc, r, p.deg[r], xb, st2, sh, tid, cnt);
+                        horner_step<Q, S>(acc, r, p.deg[r], xb, st2, sh, tid);
                     }
                     if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 5);
                     if (!STAGE) {
@@ -494,6 +650,220 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
             }
             __syncthreads();  // st2 / sh / buffers free for the next chunk
         }
+    }
+}
+
+// ---------------------------------------------------------------- TMEM variant
+// The sample role keeps its per-sample metadata in tensor memory (tmem.cuh:
+// h: 2 columns, t2: 1 column per sample), which frees the shared memory for
+// a third row buffer.
+// Triple-buffered, warp-specialized rows (L2 >= 1024):
+//   buffer b = i % 3 carries, in turn, the staged Y row of step i (cp.async by
+//   the sample warps one full step ahead), the FFT exchange of step i, and
+//   X_r of step i for the sample gathers.  Ordering: staged[b] (mbarrier,
+//   sample cp.async arrivals) -> FFT warps; FULL_b (named barrier) -> sample
+//   warps; the sample warps re-stage b only after all of them have gathered.
+//   No warp waits on a global load inside the term loop.
+template <int L2>
+struct TmShape {
+    static constexpr int G = L2 / 16;
+    static constexpr int S = 3 * G / 2;
+    static constexpr int Q = 12;  // samples per sample thread (3 chunks of 4)
+    static constexpr int CAP = Q * S;
+    static constexpr int ALL = G + S;
+    static constexpr int COLS_PER_THREAD = 3 * Q;                  // h (2 each) + t2 (1 each)
+    static constexpr int BLOCKS = (ALL / 32 + 3) / 4;              // column blocks per lane
+    static constexpr int TM_COLS = (BLOCKS * COLS_PER_THREAD <= 256) ? 256 : 512;
+    static constexpr size_t SMEM = sizeof(double2) * (3 * padded_len(L2) + FftShapeX<L2>::TW_LEN);
+    static_assert(BLOCKS * COLS_PER_THREAD <= 512, "TMEM columns");
+    static_assert(SMEM <= 227 * 1024, "pass 2 (TMEM variant) shared memory");
+    static_assert(CAP >= 18 * G, "sample capacity");
+};
+
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(TmShape<L2>::ALL, 1)
+    k2_pass2_tm(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
+    using W = TmShape<L2>;
+    constexpr int G = W::G;
+    constexpr int S = W::S;
+    constexpr int Q = W::Q;
+    constexpr int CAP = W::CAP;
+    constexpr int ALL = W::ALL;
+    constexpr int BAR_FULL = 1, BAR_FFT = 5, BAR_SMP = 6;  // FULL_b = 1..3
+    extern __shared__ double2 smem[];
+    __shared__ unsigned long long staged[3];
+    __shared__ unsigned tmem_base;
+    double2* bufs = smem;  // 3 x padded_len(L2)
+    double2* t16 = bufs + 3 * padded_len(L2);
+    const bool fft_warp = threadIdx.x < G;
+    const int tid = fft_warp ? threadIdx.x : threadIdx.x - G;
+    const int warp = threadIdx.x >> 5;
+    twiddle_table_build<L2>(t16, threadIdx.x, ALL);
+    Twiddles<L2> T;
+    if (fft_warp) twiddle_init<L2>(T, t16, tid);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init(&staged[b], S);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == G / 32) {  // first sample warp owns the TMEM allocation
+        const unsigned a = (unsigned)__cvta_generic_to_shared(&tmem_base);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a),
+                     "r"((unsigned)W::TM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's columns: block warp/4 of its lane, 3Q columns: [h lo,hi x Q][t2 x Q]
+    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((warp >> 2) * W::COLS_PER_THREAD);
+    int phase[3] = {0, 0, 0};
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        for (int cb = beg; cb < end; cb += CAP) {
+            const int cnt = min(CAP, end - cb);
+            const int nt = p.r1 - p.r0;
+            auto stage = [&](int step) {  // sample warps: Y row of `step` -> buffer step % 3
+                const int r = p.r1 - 1 - step;
+                double2* xb = bufs + (step % 3) * padded_len(L2);
+                const double2* src = Y + y_index(r - p.r0, N, p.log_n2, row, 0);
+#pragma unroll
+                for (int q = 0; q < (L2 + S - 1) / S; ++q) {
+                    const int k2 = tid + q * S;
+                    if (k2 < L2) cp_async16(xb + pad16(k2), src + 2 * k2);
+                }
+                mbar_cp_async_arrive(&staged[step % 3]);
+            };
+            if (fft_warp) {
+                for (int i = 0; i < nt; ++i) {
+                    const int b = i % 3;
+                    double2* buf = bufs + b * padded_len(L2);
+                    double2 v[16];
+                    mbar_wait(&staged[b], phase[b] & 1);
+                    ++phase[b];
+                    load_stage_input<L2>(v, buf, tid);
+                    nbar_sync(BAR_FFT, G);  // all inputs read before stage 1 reuses buf
+                    block_fft_1buf<L2, -1>(v, buf, tid, T, [] { nbar_sync(BAR_FFT, G); });
+                    nbar_sync(BAR_FFT, G);  // last-stage reads of buf done
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    nbar_arrive(BAR_FULL + b, ALL);
+                }
+            } else {
+                for (int i = 0; i < 3 && i < nt; ++i) stage(i);
+                // samples: h and t2 into TMEM, accumulators in registers
+                const double dn = (double)p.n;
+                double2 acc[Q];
+#pragma unroll
+                for (int k = 0; k < Q / 4; ++k) {
+                    double h[4];
+                    int t2[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = 4 * k + u;
+                        acc[q] = make_double2(0.0, 0.0);
+                        const int i = tid + q * S;
+                        h[u] = 0.0;
+                        t2[u] = 0;
+                        if (i < cnt) {
+                            const double x = p.xs[cb + i];
+                            const double pr = __dmul_rn(dn, x);
+                            const long long sj = (long long)round(pr);
+                            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                            t2[u] = (int)((sj & (p.n - 1)) >> p.log_n1);
+                            h[u] = half_phase(d);
+                        }
+                    }
+                    tm_st4(tcol + 8 * k, lo32(h[0]), hi32(h[0]), lo32(h[1]), hi32(h[1]));
+                    tm_st4(tcol + 8 * k + 4, lo32(h[2]), hi32(h[2]), lo32(h[3]), hi32(h[3]));
+                    tm_st4(tcol + 2 * Q + 4 * k, (unsigned)t2[0], (unsigned)t2[1], (unsigned)t2[2], (unsigned)t2[3]);
+                }
+                tm_wait_st();
+                for (int i = 0; i < nt; ++i) {
+                    const int r = p.r1 - 1 - i;
+                    const int b = i % 3;
+                    const double2* xb = bufs + b * padded_len(L2);
+                    nbar_sync(BAR_FULL + b, ALL);
+                    const double* a = kBes + r * kSeriesTerms;
+                    const int deg = p.deg[r];
+#pragma unroll
+                    for (int k = 0; k < Q / 4; ++k) {
+                        unsigned e[12];
+                        tm_ld4(tcol + 8 * k, e[0], e[1], e[2], e[3]);
+                        tm_ld4(tcol + 8 * k + 4, e[4], e[5], e[6], e[7]);
+                        tm_ld4(tcol + 2 * Q + 4 * k, e[8], e[9], e[10], e[11]);
+                        tm_wait_ld();
+                        double h[4], w[4], g[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            h[u] = mk64(e[2 * u], e[2 * u + 1]);
+                            w[u] = h[u] * h[u];
+                        }
+                        if constexpr (UNIFORM) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) acc[4 * k + u] = xb[e[8 + u]];
+                        } else {
+                            series_deg<4>(g, w, a, deg);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int q = 4 * k + u;
+                                const double2 X = xb[e[8 + u]];
+                                const double ax = acc[q].x;
+                                acc[q].x = __fma_rn(g[u], X.x, -h[u] * acc[q].y);
+                                acc[q].y = __fma_rn(g[u], X.y, h[u] * ax);
+                            }
+                        }
+                    }
+                    if (i + 3 < nt) {
+                        nbar_sync(BAR_SMP, S);  // every sample warp is done gathering from b
+                        stage(i + 3);
+                    }
+                }
+                // f[perm] = 2 exp(2ih) (ih)^r0 acc
+#pragma unroll
+                for (int k = 0; k < Q / 4; ++k) {
+                    unsigned e[8];
+                    tm_ld4(tcol + 8 * k, e[0], e[1], e[2], e[3]);
+                    tm_ld4(tcol + 8 * k + 4, e[4], e[5], e[6], e[7]);
+                    tm_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = 4 * k + u;
+                        const int i = tid + q * S;
+                        if (i >= cnt) continue;
+                        double2 out = acc[q];
+                        if constexpr (!UNIFORM) {
+                            const double h = mk64(e[2 * u], e[2 * u + 1]);
+                            if (p.r0 > 0) {
+                                double hr = 1.0;
+                                for (int m = 0; m < p.r0; ++m) hr *= h;
+                                out = cscale(out, hr);
+                                switch (p.r0 & 3) {
+                                    case 1: out = make_double2(-out.y, out.x); break;
+                                    case 2: out = make_double2(-out.x, -out.y); break;
+                                    case 3: out = make_double2(out.y, -out.x); break;
+                                    default: break;
+                                }
+                            }
+                            double sn, cs;
+                            sincos(2.0 * h, &sn, &cs);
+                            out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+                        }
+                        __stcs(f + p.perm[cb + i], out);
+                    }
+                }
+            }
+            __syncthreads();  // buffers free for the next chunk
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == G / 32) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"((unsigned)W::TM_COLS)
+                     : "memory");
     }
 }
 
@@ -520,10 +890,31 @@ int occupancy(const void* fn, int threads, size_t smem) {
     return std::max(1, n);
 }
 
+inline int pass1_variant() {
+    static const int v = [] {
+        const char* e = getenv("NUFFT_PASS1_VARIANT");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 template <int L1>
 void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int r1,
                   cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    if constexpr (L1 >= 2048) {
+        if (pass1_variant() == 1) {
+            constexpr size_t SMT = P1TmShape<L1>::SMEM;
+            Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+            auto fn = pl.uniform ? k2_pass1_tm<L1, true> : k2_pass1_tm<L1, false>;
+            set_smem(fn, SMT);
+            const long long n2 = 1ll << pl.bk.log_n2;
+            const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
+            fn<<<grid, P1TmShape<L1>::THREADS, SMT, s>>>(c, Y, p);
+            NB_LAUNCH();
+            return;
+        }
+    }
     constexpr size_t SM = pass1_smem<L1>();
     Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
     const long long n2 = 1ll << pl.bk.log_n2;
@@ -552,6 +943,17 @@ void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1,
     constexpr size_t SM = pass2_smem<L2, X2>();
     constexpr int threads = WsShape<L2, X2>::ALL;
     auto fn = k2_pass2_ws<L2, UNIFORM, X2, STAGE>;
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
+    fn<<<grid, threads, SM, s>>>(Y, f, p);
+    NB_LAUNCH();
+}
+
+template <int L2, bool UNIFORM>
+void launch_tm(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    constexpr size_t SM = TmShape<L2>::SMEM;
+    constexpr int threads = TmShape<L2>::ALL;
+    auto fn = k2_pass2_tm<L2, UNIFORM>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
     fn<<<grid, threads, SM, s>>>(Y, f, p);
@@ -589,6 +991,8 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
                       : launch_ws<L2, false, 3, false>(Y, f, p, n1, ctx.sms, s); break;
             case 3: u ? launch_ws<L2, true, 3, true>(Y, f, p, n1, ctx.sms, s)
                       : launch_ws<L2, false, 3, true>(Y, f, p, n1, ctx.sms, s); break;
+            case 4: u ? launch_tm<L2, true>(Y, f, p, n1, ctx.sms, s)
+                      : launch_tm<L2, false>(Y, f, p, n1, ctx.sms, s); break;
             default: u ? launch_ws<L2, true, 2, false>(Y, f, p, n1, ctx.sms, s)
                        : launch_ws<L2, false, 2, false>(Y, f, p, n1, ctx.sms, s); break;
         }
