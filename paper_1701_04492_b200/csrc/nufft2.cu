@@ -305,6 +305,7 @@ struct Pass2Params {
     const int* perm;
     const int* rowoff;
     unsigned long long* trace;  // diagnostics: per-iteration clock64 stamps of CTA 0 (nullptr = off)
+    int ablate;                 // diagnostics (NUFFT_ABLATE): 1 skip sample math, 2 skip FFT math
     int deg[kRankCap];
 };
 #define NB_TRACE(slot)                                                                   \
@@ -867,6 +868,229 @@ __global__ void __launch_bounds__(TmShape<L2>::ALL, 1)
     }
 }
 
+// ---------------------------------------------------------------- two FFT groups
+// Pass 2 with two FFT worker groups (steps alternate between them) and one
+// sample warpgroup whose per-sample state — accumulator, h, t2 — lives in
+// tensor memory (7 columns per sample, tmem.cuh), so all 640 threads fit in
+// 96 registers.  X_r rotates through three shared buffers (b = step % 3):
+//   FULL_b  (named barrier, producing group + sample warps): X of the step is in b;
+//   EMPTY_b (named barrier, sample warps + next user of b): the gathers from b are done.
+// Each group loads its next Y row from HBM before waiting for its buffer and
+// has two sample periods per transform, so two transforms are in flight.
+template <int L2>
+struct G2Shape {
+    static constexpr int G = L2 / 16;
+    static constexpr int S = 128;               // one sample warpgroup
+    static constexpr int Q = (18 * G / S + 3) / 4 * 4;  // samples per sample thread (capacity >= 1.125 L2)
+    static constexpr int CAP = Q * S;
+    static constexpr int ALL = 2 * G + S;
+    // TMEM columns per sample: acc (4), h (2), t2 (1), Bessel state g_r, g_{r+1} (4)
+    static constexpr int COL_ACC = 0, COL_H = 4 * Q, COL_T = 6 * Q, COL_G = 7 * Q;
+    static constexpr unsigned TM_COLS = (11 * Q <= 128) ? 128u : (11 * Q <= 256 ? 256u : 512u);
+    static constexpr size_t SMEM = sizeof(double2) * (3 * padded_len(L2) + FftShapeX<L2>::TW_LEN);
+    static_assert(Q % 4 == 0 && 11 * Q <= 512, "sample layout");
+    static_assert(SMEM <= 227 * 1024, "pass 2 (two groups) shared memory");
+};
+
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
+    k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
+    using W = G2Shape<L2>;
+    constexpr int G = W::G;
+    constexpr int S = W::S;
+    constexpr int Q = W::Q;
+    constexpr int CAP = W::CAP;
+    constexpr int PAIR = G + S;                  // FULL/EMPTY participants
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 4, BAR_GRP = 7;  // FULL 1..3, EMPTY 4..6, groups 7..8
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    double2* bufs = smem;
+    double2* t16 = bufs + 3 * padded_len(L2);
+    const int role = threadIdx.x < 2 * G ? threadIdx.x / G : 2;  // 0, 1: FFT groups; 2: samples
+    const int tid = role < 2 ? threadIdx.x - role * G : threadIdx.x - 2 * G;
+    twiddle_table_build<L2>(t16, threadIdx.x, W::ALL);
+    Twiddles<L2> T;
+    twiddle_init<L2>(T, t16, tid);
+    if (role == 2 && tid < 32) tm_alloc(&tmem_base, W::TM_COLS);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tl = tm_lane_base(tmem_base);  // sample warps 2G/32.. map to quarters 0..3
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const long long n2 = 1ll << p.log_n2;
+    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        for (int cb = beg; cb < end; cb += CAP) {
+            const int cnt = min(CAP, end - cb);
+            const int nt = p.r1 - p.r0;
+            if (role < 2) {
+                const int bar = BAR_GRP + role;
+                auto gsync = [bar] { nbar_sync(bar, G); };
+                for (int i = role; i < nt; i += 2) {
+                    const int b = i % 3;
+                    double2* buf = bufs + b * padded_len(L2);
+                    const int rr = p.r1 - 1 - i - p.r0;
+                    if (tid == 0 && i + 2 < nt) {  // warm L2 with this group's next row
+                        const void* nxt = Y + y_index(rr - 2, N, p.log_n2, row, 0);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                                     "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
+                    }
+                    const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
+                    double2 v[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
+                    if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                    gsync();  // last-stage reads of buf done
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    nbar_arrive(BAR_FULL + b, PAIR);
+                }
+            } else {
+                const double dn = (double)p.n;
+                // per-sample state into TMEM: acc = 0, h, t2
+#pragma unroll 1
+                for (int k = 0; k < Q / 4; ++k) {
+                    unsigned av[16], hv[8];
+                    unsigned t2v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = tid + (4 * k + u) * S;
+                        double h = 0.0;
+                        int t2 = 0;
+                        if (i < cnt) {
+                            const double x = p.xs[cb + i];
+                            const double pr = __dmul_rn(dn, x);
+                            const long long sj = (long long)round(pr);
+                            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                            t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
+                            h = half_phase(d);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
+                        hv[2 * u] = lo32(h);
+                        hv[2 * u + 1] = hi32(h);
+                        t2v[u] = (unsigned)t2;
+                    }
+                    tm_st16(tl + W::COL_ACC + 16 * k, av);
+                    tm_st8(tl + W::COL_H + 8 * k, hv);
+                    tm_st4(tl + W::COL_T + 4 * k, t2v[0], t2v[1], t2v[2], t2v[3]);
+                    if constexpr (!UNIFORM) {
+                        // (g_{r1-1}, g_{r1}) by the full series; lower orders follow from
+                        // the backward recurrence g_{r-1} = r g_r - w g_{r+1}, stable for
+                        // the minimal (Bessel) solution
+                        double w[4], ga[4], gb[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                            w[u] = h * h;
+                        }
+                        series_fixed<4, kSeriesTerms - 1>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms);
+                        series_fixed<4, kSeriesTerms - 1>(gb, w, kBes + p.r1 * kSeriesTerms);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            av[4 * u] = lo32(ga[u]);
+                            av[4 * u + 1] = hi32(ga[u]);
+                            av[4 * u + 2] = lo32(gb[u]);
+                            av[4 * u + 3] = hi32(gb[u]);
+                        }
+                        tm_st16(tl + W::COL_G + 16 * k, av);
+                    }
+                }
+                tm_wait_st();
+                for (int i = 0; i < nt; ++i) {
+                    const int r = p.r1 - 1 - i;
+                    const int b = i % 3;
+                    const double2* xb = bufs + b * padded_len(L2);
+                    nbar_sync(BAR_FULL + b, PAIR);
+                    const double* a = kBes + r * kSeriesTerms;
+                    const int deg = p.deg[r];
+                    (void)a;
+                    (void)deg;
+                    const double rd = (double)r;
+#pragma unroll 1
+                    for (int k = 0; k < ((p.ablate & 1) ? 0 : Q / 4); ++k) {
+                        unsigned av[16], gv[16], hv[8], t2v[4];
+                        tm_ld16(tl + W::COL_ACC + 16 * k, av);
+                        tm_ld8(tl + W::COL_H + 8 * k, hv);
+                        tm_ld4(tl + W::COL_T + 4 * k, t2v[0], t2v[1], t2v[2], t2v[3]);
+                        if constexpr (!UNIFORM) tm_ld16(tl + W::COL_G + 16 * k, gv);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const double2 X = xb[t2v[u]];
+                            double2 acc;
+                            if constexpr (UNIFORM) {
+                                acc = X;
+                            } else {
+                                const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                                const double gr = mk64(gv[4 * u], gv[4 * u + 1]);
+                                const double gr1 = mk64(gv[4 * u + 2], gv[4 * u + 3]);
+                                const double ax = mk64(av[4 * u], av[4 * u + 1]);
+                                const double ay = mk64(av[4 * u + 2], av[4 * u + 3]);
+                                acc.x = __fma_rn(gr, X.x, -h * ay);
+                                acc.y = __fma_rn(gr, X.y, h * ax);
+                                const double gm1 = __fma_rn(rd, gr, -(h * h) * gr1);  // g_{r-1}
+                                gv[4 * u] = lo32(gm1);
+                                gv[4 * u + 1] = hi32(gm1);
+                                gv[4 * u + 2] = lo32(gr);
+                                gv[4 * u + 3] = hi32(gr);
+                            }
+                            av[4 * u] = lo32(acc.x);
+                            av[4 * u + 1] = hi32(acc.x);
+                            av[4 * u + 2] = lo32(acc.y);
+                            av[4 * u + 3] = hi32(acc.y);
+                        }
+                        tm_st16(tl + W::COL_ACC + 16 * k, av);
+                        if constexpr (!UNIFORM) tm_st16(tl + W::COL_G + 16 * k, gv);
+                    }
+                    // release b only to a later step (an EMPTY arrival nobody waits
+                    // for would pair with the next use of the barrier)
+                    if (i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
+                }
+                tm_wait_st();
+                // f[perm] = 2 exp(2ih) (ih)^r0 acc
+#pragma unroll 1
+                for (int k = 0; k < Q / 4; ++k) {
+                    unsigned av[16], hv[8];
+                    tm_ld16(tl + W::COL_ACC + 16 * k, av);
+                    tm_ld8(tl + W::COL_H + 8 * k, hv);
+                    tm_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = tid + (4 * k + u) * S;
+                        if (i >= cnt) continue;
+                        double2 out = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+                        if constexpr (!UNIFORM) {
+                            const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                            if (p.r0 > 0) {
+                                double hr = 1.0;
+                                for (int m = 0; m < p.r0; ++m) hr *= h;
+                                out = cscale(out, hr);
+                                switch (p.r0 & 3) {
+                                    case 1: out = make_double2(-out.y, out.x); break;
+                                    case 2: out = make_double2(-out.x, -out.y); break;
+                                    case 3: out = make_double2(out.y, -out.x); break;
+                                    default: break;
+                                }
+                            }
+                            double sn, cs;
+                            sincos(2.0 * h, &sn, &cs);
+                            out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+                        }
+                        __stcs(f + p.perm[cb + i], out);
+                    }
+                }
+            }
+            __syncthreads();  // buffers and TMEM state free for the next chunk
+        }
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (role == 2 && tid < 32) tm_dealloc(tmem_base, W::TM_COLS);
+}
+
 // ------------------------------------------------------------------ launch
 template <int L>
 constexpr size_t pass1_smem() {
@@ -925,14 +1149,19 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
     NB_LAUNCH();
 }
 
-// pass-2 organization for rows >= 1024 (sample-role width X2/2 of the FFT
-// role, Y staging on/off); NUFFT_PASS2_VARIANT selects one for experiments
-// (0: X2=2 no staging, 1: X2=2 staged, 2: X2=3 no staging [default],
-//  3: X2=3 staged) — measured on B200 at N=2^24: 3.45 / 4.41 / 3.36 / 3.89 ms
+// pass-2 organization for rows >= 1024; NUFFT_PASS2_VARIANT selects one for
+// experiments.  Measured on B200 at N = 2^24, K = 20 (pass-2 ms):
+//   0: one FFT group, X2=2 sample width             3.36
+//   1: as 0, Y rows staged by the sample warps      3.87
+//   2: one FFT group, X2=3                          3.23
+//   3: as 2, staged                                 3.81
+//   4: one FFT group, TMEM sample metadata, 3 bufs  3.37
+//   5: two FFT groups, TMEM sample state, Bessel
+//      backward recurrence (L2 >= 2048) [default]   3.05
 inline int pass2_variant() {
     static const int v = [] {
         const char* e = getenv("NUFFT_PASS2_VARIANT");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 5;
     }();
     return v;
 }
@@ -945,6 +1174,17 @@ void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1,
     auto fn = k2_pass2_ws<L2, UNIFORM, X2, STAGE>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
+    fn<<<grid, threads, SM, s>>>(Y, f, p);
+    NB_LAUNCH();
+}
+
+template <int L2, bool UNIFORM>
+void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    constexpr size_t SM = G2Shape<L2>::SMEM;
+    constexpr int threads = G2Shape<L2>::ALL;
+    auto fn = k2_pass2_g2<L2, UNIFORM>;
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);
     NB_LAUNCH();
 }
@@ -975,6 +1215,8 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
     static const bool trace = getenv("NUFFT_TRACE_PASS2") != nullptr;
+    static const int ablate = getenv("NUFFT_ABLATE") ? atoi(getenv("NUFFT_ABLATE")) : 0;
+    p.ablate = ablate;
     unsigned long long* tr = nullptr;
     if (trace) {
         NB_CUDA(cudaMalloc(&tr, 8 * 8 * 64));
@@ -993,6 +1235,14 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
                       : launch_ws<L2, false, 3, true>(Y, f, p, n1, ctx.sms, s); break;
             case 4: u ? launch_tm<L2, true>(Y, f, p, n1, ctx.sms, s)
                       : launch_tm<L2, false>(Y, f, p, n1, ctx.sms, s); break;
+            case 5:
+                if constexpr (L2 >= 2048) {
+                    u ? launch_g2<L2, true>(Y, f, p, n1, ctx.sms, s) : launch_g2<L2, false>(Y, f, p, n1, ctx.sms, s);
+                } else {
+                    u ? launch_ws<L2, true, 3, false>(Y, f, p, n1, ctx.sms, s)
+                      : launch_ws<L2, false, 3, false>(Y, f, p, n1, ctx.sms, s);
+                }
+                break;
             default: u ? launch_ws<L2, true, 2, false>(Y, f, p, n1, ctx.sms, s)
                        : launch_ws<L2, false, 2, false>(Y, f, p, n1, ctx.sms, s); break;
         }

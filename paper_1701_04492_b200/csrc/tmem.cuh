@@ -44,6 +44,17 @@ __device__ __forceinline__ void tm_ld4(unsigned taddr, unsigned& a, unsigned& b,
                  : "r"(taddr)
                  : "memory");
 }
+__device__ __forceinline__ void tm_st8(unsigned taddr, const unsigned (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld8(unsigned taddr, unsigned (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
 // 16 consecutive columns
 __device__ __forceinline__ void tm_st16(unsigned taddr, const unsigned (&v)[16]) {
     asm volatile(
