@@ -251,6 +251,16 @@ inline ComplexVector exec_nufft1(const Plan1& plan, const ComplexVector& c) {
     return f;
 }
 
+namespace detail {
+/// F1~* g = conj(F2~ conj(g)) on the inner plan (transforms.hpp:294-300)
+inline ComplexVector exec_nufft1_adjoint(const Plan1& plan, const ComplexVector& g) {
+    if (g.size() != plan.size()) throw std::invalid_argument("nufft transpose: length mismatch");
+    ComplexVector out(g.size());
+    check(nufft_plan1_adjoint_host(plan.device.get(), dp(g), g.size(), dp(out)));
+    return out;
+}
+}  // namespace detail
+
 /// Type-III plan (transforms.hpp:308-319).
 struct Plan3 {
     SampleSet samples;

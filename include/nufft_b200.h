@@ -146,6 +146,44 @@ int nufft_plan1_exec(const nufft_plan1* plan, const double* c_dev, double* f_dev
                      void* stream);                                       /* transforms.hpp:287-289 */
 int nufft_plan1_exec_host(const nufft_plan1* plan, const double* c, size_t len, double* f,
                           size_t batch);
+/* F1~* g = conj(F2~ conj(g)) on the inner plan (detail::exec_nufft1_adjoint transforms.hpp:294-300) */
+int nufft_plan1_adjoint(const nufft_plan1* plan, const double* g_dev, double* out_dev, void* stream);
+int nufft_plan1_adjoint_host(const nufft_plan1* plan, const double* g, size_t len, double* out);
+
+/* ------------------------------------------------------------- inverse (inverse.hpp) */
+typedef struct nufft_toeplitz nufft_toeplitz; /* ToeplitzOperator inverse.hpp:22-27 */
+/* CgReport inverse.hpp:89-95; the solution and residualHistory go to caller buffers */
+typedef struct nufft_cg_report {
+    size_t iterations;
+    double relative_residual;
+    int converged;
+    size_t history_len; /* entries written to the history buffer (min(iterations, cap)) */
+} nufft_cg_report;
+/* detail::toeplitz_from_first_column inverse.hpp:37-50 (column: n complex, host) */
+int nufft_toeplitz_from_first_column(const double* column, size_t n, int device, nufft_toeplitz** out);
+int nufft_toeplitz_from_normal(const nufft_plan2* plan, nufft_toeplitz** out); /* inverse.hpp:54-58 */
+int nufft_toeplitz_from_gram(const nufft_plan1* plan, nufft_toeplitz** out);   /* inverse.hpp:61-66 */
+void nufft_toeplitz_destroy(nufft_toeplitz* op);
+int nufft_toeplitz_size(const nufft_toeplitz* op, size_t* n);
+/* members: spectrum 2n complex (imaginary parts 0), firstColumn n complex; NULL skips */
+int nufft_toeplitz_members(const nufft_toeplitz* op, double* spectrum, double* first_column);
+int nufft_toeplitz_matvec(const nufft_toeplitz* op, const double* v_dev, double* out_dev,
+                          void* stream);                                   /* inverse.hpp:70-85 */
+int nufft_toeplitz_matvec_host(const nufft_toeplitz* op, const double* v, size_t len, double* out);
+/* cg_solve inverse.hpp:118-157 with the Toeplitz matvec as the operator */
+int nufft_cg_toeplitz_host(const nufft_toeplitz* op, const double* rhs, size_t len, double tol,
+                           size_t max_iter, double* solution, nufft_cg_report* report,
+                           double* history, size_t history_cap);
+/* inufft2 inverse.hpp:171-183 / inufft1 :187-200; op NULL = built from the plan */
+int nufft_inufft2_host(const nufft_plan2* plan, const nufft_toeplitz* op, const double* f, size_t len,
+                       double tol, double* solution, nufft_cg_report* report, double* history,
+                       size_t history_cap);
+int nufft_inufft2(const nufft_plan2* plan, const nufft_toeplitz* op, const double* f_dev, double tol,
+                  double* solution_dev, nufft_cg_report* report, void* stream);
+int nufft_inufft1_host(const nufft_plan1* plan, const nufft_toeplitz* op, const double* f, size_t len,
+                       double tol, double* solution, nufft_cg_report* report, double* history,
+                       size_t history_cap);
+size_t nufft_default_cg_max_iter(size_t n); /* detail::default_cg_max_iter inverse.hpp:161-164 */
 
 /* ------------------------------------------------------------- type III */
 int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, size_t n_omega,

@@ -1076,3 +1076,229 @@ void orc_sampler_complex_vector(void* s, size_t n, double* out) {
         out[2 * i + 1] = orc_sampler_normal(s);
     }
 }
+
+/* -------------------------------------------------------- inverse.hpp */
+/* F1~* g = conj(F2~ conj(g)) on the inner plan (transforms.hpp:294-300) */
+int orc_plan1_adjoint(void* p, const double* g_in, double* out) {
+    const orc_plan1* P = (const orc_plan1*)p;
+    const size_t n = P->n;
+    cplx* tmp = (cplx*)malloc(sizeof(cplx) * n);
+    for (size_t j = 0; j < n; ++j) tmp[j] = cconj(((const cplx*)g_in)[j]);
+    orc_plan2_exec(P->inner, (const double*)tmp, out, 1);
+    for (size_t j = 0; j < n; ++j) ((cplx*)out)[j] = cconj(((cplx*)out)[j]);
+    free(tmp);
+    return 0;
+}
+
+typedef struct {
+    size_t n;
+    cplx* spectrum;  /* 2n, imaginary parts truncated */
+    cplx* first_col; /* n */
+} orc_toeplitz;
+
+void orc_toeplitz_destroy(void* p) {
+    orc_toeplitz* T = (orc_toeplitz*)p;
+    if (!T) return;
+    free(T->spectrum);
+    free(T->first_col);
+    free(T);
+}
+
+/* detail::toeplitz_from_first_column inverse.hpp:37-50 */
+int orc_toeplitz_column(const double* col_in, size_t n, void** out) {
+    const cplx* col = (const cplx*)col_in;
+    const size_t n2 = 2 * n;
+    orc_toeplitz* T = (orc_toeplitz*)calloc(1, sizeof(orc_toeplitz));
+    T->n = n;
+    T->first_col = (cplx*)malloc(sizeof(cplx) * n);
+    memcpy(T->first_col, col, sizeof(cplx) * n);
+    cplx* symbol = (cplx*)calloc(n2, sizeof(cplx));
+    for (size_t j = 0; j < n; ++j) symbol[j] = col[j];
+    for (size_t j = 1; j < n; ++j) symbol[n2 - j] = cconj(col[j]);
+    T->spectrum = (cplx*)malloc(sizeof(cplx) * n2);
+    fft_fwd((int)n2, symbol, T->spectrum);
+    for (size_t j = 0; j < n2; ++j) T->spectrum[j].im = 0.0;
+    free(symbol);
+    orc_fft_plan_for((int)n2);
+    *out = T;
+    return 0;
+}
+
+/* toeplitz_from_normal inverse.hpp:54-58: first column F2~* F2~ e_0 */
+int orc_toeplitz_normal(void* plan2, void** out) {
+    const orc_plan2* P = (const orc_plan2*)plan2;
+    const size_t n = P->n;
+    cplx* e0 = (cplx*)calloc(n, sizeof(cplx));
+    cplx* f = (cplx*)malloc(sizeof(cplx) * n);
+    cplx* col = (cplx*)malloc(sizeof(cplx) * n);
+    e0[0].re = 1.0;
+    orc_plan2_exec(plan2, (const double*)e0, (double*)f, 1);
+    orc_plan2_adjoint(plan2, (const double*)f, (double*)col);
+    int rc = orc_toeplitz_column((const double*)col, n, out);
+    free(e0);
+    free(f);
+    free(col);
+    return rc;
+}
+
+/* toeplitz_from_gram inverse.hpp:61-66: first column F1~ F1~* e_0 */
+int orc_toeplitz_gram(void* plan1, void** out) {
+    const orc_plan1* P = (const orc_plan1*)plan1;
+    const size_t n = P->n;
+    cplx* e0 = (cplx*)calloc(n, sizeof(cplx));
+    cplx* g = (cplx*)malloc(sizeof(cplx) * n);
+    cplx* col = (cplx*)malloc(sizeof(cplx) * n);
+    e0[0].re = 1.0;
+    orc_plan1_adjoint(plan1, (const double*)e0, (double*)g);
+    orc_plan1_exec(plan1, (const double*)g, (double*)col);
+    int rc = orc_toeplitz_column((const double*)col, n, out);
+    free(e0);
+    free(g);
+    free(col);
+    return rc;
+}
+
+int orc_toeplitz_members(void* p, double* spectrum, double* first_col) {
+    const orc_toeplitz* T = (const orc_toeplitz*)p;
+    if (spectrum) memcpy(spectrum, T->spectrum, sizeof(cplx) * 2 * T->n);
+    if (first_col) memcpy(first_col, T->first_col, sizeof(cplx) * T->n);
+    return 0;
+}
+
+/* toeplitz_matvec inverse.hpp:70-85 */
+static void toeplitz_apply(const orc_toeplitz* T, const cplx* v, cplx* out) {
+    const size_t n = T->n, n2 = 2 * n;
+    cplx* padded = (cplx*)calloc(n2, sizeof(cplx));
+    cplx* spec = (cplx*)malloc(sizeof(cplx) * n2);
+    cplx* back = (cplx*)malloc(sizeof(cplx) * n2);
+    for (size_t j = 0; j < n; ++j) padded[j] = v[j];
+    fft_fwd((int)n2, padded, spec);
+    for (size_t j = 0; j < n2; ++j) spec[j] = cscale(spec[j], T->spectrum[j].re);
+    fft_bwd_raw((int)n2, spec, back);
+    const double scale = 1.0 / (double)n2;
+    for (size_t j = 0; j < n; ++j) out[j] = cscale(back[j], scale);
+    free(padded);
+    free(spec);
+    free(back);
+}
+int orc_toeplitz_matvec(void* p, const double* v, size_t len, double* out) {
+    const orc_toeplitz* T = (const orc_toeplitz*)p;
+    if (len != T->n) FAIL(1, "toeplitz_matvec: length mismatch");
+    toeplitz_apply(T, (const cplx*)v, (cplx*)out);
+    return 0;
+}
+
+size_t orc_default_cg_max_iter(size_t n) { /* inverse.hpp:161-164 */
+    const size_t sqrt_n = (size_t)ceil(sqrt((double)n));
+    return 4 * sqrt_n > 100 ? 4 * sqrt_n : 100;
+}
+
+static double dot_real(const cplx* a, const cplx* b, size_t n) { /* inverse.hpp:105-111 */
+    double s = 0.0;
+    for (size_t j = 0; j < n; ++j) s += a[j].re * b[j].re + a[j].im * b[j].im;
+    return s;
+}
+static double norm2(const cplx* v, size_t n) { /* inverse.hpp:99-103 (std::norm = re^2 + im^2) */
+    double s = 0.0;
+    for (size_t j = 0; j < n; ++j) s += v[j].re * v[j].re + v[j].im * v[j].im;
+    return sqrt(s);
+}
+
+/* cg_solve inverse.hpp:118-157 with the Toeplitz matvec */
+int orc_cg_toeplitz(void* op, const double* rhs_in, size_t n, double tol, size_t max_iter, double* sol_out,
+                    size_t* iters, double* relres, int* converged, double* history, size_t* hist_len) {
+    const orc_toeplitz* T = (const orc_toeplitz*)op;
+    if (!(tol > 0.0)) FAIL(2, "cg_solve: tol must be positive");
+    const cplx* rhs = (const cplx*)rhs_in;
+    cplx* x = (cplx*)sol_out;
+    memset(x, 0, sizeof(cplx) * n);
+    *iters = 0;
+    *relres = 0.0;
+    *converged = 0;
+    *hist_len = 0;
+    const double rhs_norm = norm2(rhs, n);
+    if (rhs_norm == 0.0) {
+        *converged = 1;
+        return 0;
+    }
+    cplx* r = (cplx*)malloc(sizeof(cplx) * n);
+    cplx* p = (cplx*)malloc(sizeof(cplx) * n);
+    cplx* ap = (cplx*)malloc(sizeof(cplx) * n);
+    memcpy(r, rhs, sizeof(cplx) * n);
+    memcpy(p, r, sizeof(cplx) * n);
+    double rho = dot_real(r, r, n);
+    int done = 0;
+    for (size_t it = 1; it <= max_iter; ++it) {
+        toeplitz_apply(T, p, ap);
+        const double denom = dot_real(p, ap, n);
+        if (denom <= 0.0) break;
+        const double alpha = rho / denom;
+        for (size_t j = 0; j < n; ++j) {
+            x[j] = cadd(x[j], cscale(p[j], alpha));
+            r[j].re -= alpha * ap[j].re;
+            r[j].im -= alpha * ap[j].im;
+        }
+        const double rho_next = dot_real(r, r, n);
+        *iters = it;
+        *relres = sqrt(rho_next) / rhs_norm;
+        if (history) history[*hist_len] = *relres;
+        ++*hist_len;
+        if (*relres <= tol) {
+            *converged = 1;
+            done = 1;
+            break;
+        }
+        const double beta = rho_next / rho;
+        for (size_t j = 0; j < n; ++j) p[j] = cadd(r[j], cscale(p[j], beta));
+        rho = rho_next;
+    }
+    if (!done) *relres = sqrt(rho) / rhs_norm;
+    free(r);
+    free(p);
+    free(ap);
+    return 0;
+}
+
+/* inufft2 inverse.hpp:171-183 (op NULL: built from the plan) */
+int orc_inufft2(void* plan2, void* op, const double* f, double tol, double* sol, size_t* iters, double* relres,
+                int* converged, double* history, size_t* hist_len) {
+    const orc_plan2* P = (const orc_plan2*)plan2;
+    void* own = NULL;
+    if (!op) {
+        orc_toeplitz_normal(plan2, &own);
+        op = own;
+    }
+    if (!(P->gamma < 0.5)) {
+        orc_toeplitz_destroy(own);
+        FAIL(2, "inufft2: gamma >= 1/2, samples may not be distinct");
+    }
+    cplx* rhs = (cplx*)malloc(sizeof(cplx) * P->n);
+    orc_plan2_adjoint(plan2, f, (double*)rhs);
+    int rc = orc_cg_toeplitz(op, (const double*)rhs, P->n, tol, orc_default_cg_max_iter(P->n), sol, iters, relres,
+                             converged, history, hist_len);
+    free(rhs);
+    orc_toeplitz_destroy(own);
+    return rc;
+}
+
+/* inufft1 inverse.hpp:187-200 */
+int orc_inufft1(void* plan1, void* op, const double* f, double tol, double* sol, size_t* iters, double* relres,
+                int* converged, double* history, size_t* hist_len) {
+    const orc_plan1* P = (const orc_plan1*)plan1;
+    void* own = NULL;
+    if (!op) {
+        orc_toeplitz_gram(plan1, &own);
+        op = own;
+    }
+    if (!(P->inner->gamma < 0.5)) {
+        orc_toeplitz_destroy(own);
+        FAIL(2, "inufft1: gamma >= 1/2, frequencies may not be distinct");
+    }
+    cplx* y = (cplx*)malloc(sizeof(cplx) * P->n);
+    int rc = orc_cg_toeplitz(op, f, P->n, tol, orc_default_cg_max_iter(P->n), (double*)y, iters, relres, converged,
+                             history, hist_len);
+    if (!rc) orc_plan1_adjoint(plan1, (const double*)y, sol);
+    free(y);
+    orc_toeplitz_destroy(own);
+    return rc;
+}

@@ -91,6 +91,20 @@ class Oracle:
         self._p1rank = fn("plan1_rank", _sz, [_vp])
         self._p1gamma = fn("plan1_gamma", C.c_double, [_vp])
         self._p1e = fn("plan1_exec", C.c_int, [_vp, _dp, _dp])
+        self._p1adj = fn("plan1_adjoint", C.c_int, [_vp, _dp, _dp])
+        self._tcol = fn("toeplitz_column", C.c_int, [_dp, _sz, C.POINTER(_vp)])
+        self._tnorm = fn("toeplitz_normal", C.c_int, [_vp, C.POINTER(_vp)])
+        self._tgram = fn("toeplitz_gram", C.c_int, [_vp, C.POINTER(_vp)])
+        self._tdel = fn("toeplitz_destroy", None, [_vp])
+        self._tmem = fn("toeplitz_members", C.c_int, [_vp, _dp, _dp])
+        self._tmv = fn("toeplitz_matvec", C.c_int, [_vp, _dp, _sz, _dp])
+        self._cgmax = fn("default_cg_max_iter", _sz, [_sz])
+        cg_args = [_dp, C.c_double, _dp, C.POINTER(_sz), C.POINTER(C.c_double), C.POINTER(C.c_int), _dp,
+                   C.POINTER(_sz)]
+        self._cgt = fn("cg_toeplitz", C.c_int, [_vp, _dp, _sz, C.c_double, _sz, _dp, C.POINTER(_sz),
+                                                C.POINTER(C.c_double), C.POINTER(C.c_int), _dp, C.POINTER(_sz)])
+        self._inv2 = fn("inufft2", C.c_int, [_vp, _vp] + cg_args)
+        self._inv1 = fn("inufft1", C.c_int, [_vp, _vp] + cg_args)
         self._p3c = fn("plan3_create", C.c_int, [_dp, _dp, _sz, C.c_double, C.POINTER(_vp)])
         self._p3d = fn("plan3_destroy", None, [_vp])
         self._p3info = fn("plan3_info", C.c_int,
@@ -230,6 +244,84 @@ class Oracle:
     def sampler(self, seed: int) -> "_Sampler":
         return _Sampler(self, seed)
 
+    # ------------------------------------------------------------ inverse.hpp
+    def toeplitz_from_first_column(self, col) -> "_Toeplitz":
+        col = np.ascontiguousarray(col, np.complex128)
+        h = _vp()
+        self._check(self._tcol(_c2(col), len(col), C.byref(h)))
+        return _Toeplitz(self, h, len(col))
+
+    def toeplitz_from_normal(self, plan) -> "_Toeplitz":
+        h = _vp()
+        self._check(self._tnorm(plan.h, C.byref(h)))
+        return _Toeplitz(self, h, plan.n)
+
+    def toeplitz_from_gram(self, plan) -> "_Toeplitz":
+        h = _vp()
+        self._check(self._tgram(plan.h, C.byref(h)))
+        return _Toeplitz(self, h, plan.n)
+
+    def default_cg_max_iter(self, n: int) -> int:
+        return self._cgmax(n)
+
+    def _cg_call(self, f, n, *head):
+        sol = np.zeros(n, np.complex128)
+        cap = max(self.default_cg_max_iter(n), 1) + 1
+        hist = np.zeros(cap)
+        it, rr, cv, hl = _sz(), C.c_double(), C.c_int(), _sz()
+        self._check(f(*head, sol.view(np.float64), C.byref(it), C.byref(rr), C.byref(cv), hist, C.byref(hl)))
+        return {"solution": sol, "iterations": it.value, "relativeResidual": rr.value,
+                "converged": bool(cv.value), "residualHistory": hist[:hl.value].copy()}
+
+    def cg_toeplitz(self, op, rhs, tol, max_iter):
+        rhs = np.ascontiguousarray(rhs, np.complex128)
+        sol = np.zeros(len(rhs), np.complex128)
+        hist = np.zeros(max_iter + 1)
+        it, rr, cv, hl = _sz(), C.c_double(), C.c_int(), _sz()
+        self._check(self._cgt(op.h, _c2(rhs), len(rhs), tol, max_iter, sol.view(np.float64), C.byref(it),
+                              C.byref(rr), C.byref(cv), hist, C.byref(hl)))
+        return {"solution": sol, "iterations": it.value, "relativeResidual": rr.value,
+                "converged": bool(cv.value), "residualHistory": hist[:hl.value].copy()}
+
+    def inufft2(self, plan, f, tol, op=None):
+        f = np.ascontiguousarray(f, np.complex128)
+        return self._cg_call(self._inv2, plan.n, plan.h, op.h if op else None, _c2(f), tol)
+
+    def inufft1(self, plan, f, tol, op=None):
+        f = np.ascontiguousarray(f, np.complex128)
+        return self._cg_call(self._inv1, plan.n, plan.h, op.h if op else None, _c2(f), tol)
+
+
+class _Toeplitz:
+    def __init__(self, o: Oracle, h, n: int):
+        self.o, self.h, self.n = o, h, n
+
+    def __del__(self):
+        try:
+            self.o._tdel(self.h)
+        except Exception:
+            pass
+
+    def _members(self):
+        sp = np.zeros(2 * self.n, np.complex128)
+        fc = np.zeros(self.n, np.complex128)
+        self.o._check(self.o._tmem(self.h, sp.view(np.float64), fc.view(np.float64)))
+        return sp, fc
+
+    @property
+    def spectrum(self) -> np.ndarray:
+        return self._members()[0]
+
+    @property
+    def firstColumn(self) -> np.ndarray:  # noqa: N802 (reference member name)
+        return self._members()[1]
+
+    def matvec(self, v) -> np.ndarray:
+        v = np.ascontiguousarray(v, np.complex128)
+        out = np.zeros(len(v), np.complex128)
+        self.o._check(self.o._tmv(self.h, _c2(v), len(v), out.view(np.float64)))
+        return out
+
 
 class _Sampler:
     def __init__(self, o: Oracle, seed: int):
@@ -351,7 +443,8 @@ class _Plan:
     def adjoint(self, f) -> np.ndarray:
         f = np.ascontiguousarray(f, np.complex128)
         out = np.zeros(self.n, np.complex128)
-        self.o._check(self.o._p2adj(self.h, _c2(f), out.view(np.float64)))
+        adj = self.o._p1adj if self.kind == "1" else self.o._p2adj
+        self.o._check(adj(self.h, _c2(f), out.view(np.float64)))
         return out
 
 

@@ -178,6 +178,73 @@ int ref_plan1_exec(void* p, const double* c, double* f) {
     });
 }
 
+int ref_plan1_adjoint(void* p, const double* g, double* out) {
+    return guard([&] {
+        auto* P = static_cast<Plan1*>(p);
+        put(detail::exec_nufft1_adjoint(*P, cvec(g, P->size())), out);
+    });
+}
+
+// ---- inverse (inverse.hpp) ---------------------------------------------
+int ref_toeplitz_column(const double* col, size_t n, void** out) {
+    return guard([&] { *out = new ToeplitzOperator(detail::toeplitz_from_first_column(cvec(col, n))); });
+}
+int ref_toeplitz_normal(void* plan2, void** out) {
+    return guard([&] { *out = new ToeplitzOperator(toeplitz_from_normal(*static_cast<Plan2*>(plan2))); });
+}
+int ref_toeplitz_gram(void* plan1, void** out) {
+    return guard([&] { *out = new ToeplitzOperator(toeplitz_from_gram(*static_cast<Plan1*>(plan1))); });
+}
+void ref_toeplitz_destroy(void* p) { delete static_cast<ToeplitzOperator*>(p); }
+int ref_toeplitz_members(void* p, double* spectrum, double* first_col) {
+    return guard([&] {
+        auto* T = static_cast<ToeplitzOperator*>(p);
+        if (spectrum) put(T->spectrum, spectrum);
+        if (first_col) put(T->firstColumn, first_col);
+    });
+}
+int ref_toeplitz_matvec(void* p, const double* v, size_t len, double* out) {
+    return guard([&] { put(toeplitz_matvec(*static_cast<ToeplitzOperator*>(p), cvec(v, len)), out); });
+}
+size_t ref_default_cg_max_iter(size_t n) { return detail::default_cg_max_iter(n); }
+static void put_report(const CgReport& r, double* sol, size_t* iters, double* relres, int* conv, double* hist,
+                       size_t* hist_len) {
+    put(r.solution, sol);
+    *iters = r.iterations;
+    *relres = r.relativeResidual;
+    *conv = r.converged ? 1 : 0;
+    *hist_len = r.residualHistory.size();
+    if (hist && !r.residualHistory.empty())
+        std::memcpy(hist, r.residualHistory.data(), sizeof(double) * r.residualHistory.size());
+}
+int ref_cg_toeplitz(void* op, const double* rhs, size_t n, double tol, size_t max_iter, double* sol, size_t* iters,
+                    double* relres, int* conv, double* hist, size_t* hist_len) {
+    return guard([&] {
+        auto* T = static_cast<ToeplitzOperator*>(op);
+        const CgReport r = cg_solve([T](const ComplexVector& v) { return toeplitz_matvec(*T, v); }, cvec(rhs, n), tol,
+                                    max_iter);
+        put_report(r, sol, iters, relres, conv, hist, hist_len);
+    });
+}
+int ref_inufft2(void* plan2, void* op, const double* f, double tol, double* sol, size_t* iters, double* relres,
+                int* conv, double* hist, size_t* hist_len) {
+    return guard([&] {
+        auto* P = static_cast<Plan2*>(plan2);
+        const CgReport r = op ? inufft2(*P, *static_cast<ToeplitzOperator*>(op), cvec(f, P->size()), tol)
+                              : inufft2(*P, cvec(f, P->size()), tol);
+        put_report(r, sol, iters, relres, conv, hist, hist_len);
+    });
+}
+int ref_inufft1(void* plan1, void* op, const double* f, double tol, double* sol, size_t* iters, double* relres,
+                int* conv, double* hist, size_t* hist_len) {
+    return guard([&] {
+        auto* P = static_cast<Plan1*>(plan1);
+        const CgReport r = op ? inufft1(*P, *static_cast<ToeplitzOperator*>(op), cvec(f, P->size()), tol)
+                              : inufft1(*P, cvec(f, P->size()), tol);
+        put_report(r, sol, iters, relres, conv, hist, hist_len);
+    });
+}
+
 // ---- type III ----------------------------------------------------------
 int ref_plan3_create(const double* x, const double* omega, size_t n, double eps, void** out) {
     return guard([&] { *out = new Plan3(plan_nufft3(vec(x, n), vec(omega, n), eps)); });

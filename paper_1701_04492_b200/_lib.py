@@ -24,6 +24,11 @@ class PlanInfo(C.Structure):
     ]
 
 
+class CgReport(C.Structure):
+    _fields_ = [("iterations", _sz), ("relative_residual", C.c_double), ("converged", _i),
+                ("history_len", _sz)]
+
+
 _SIGS = {
     "nufft_last_error": (C.c_char_p, []),
     "nufft_abi_version": (_i, []),
@@ -65,6 +70,21 @@ _SIGS = {
     "nufft_plan1_samples": (_i, [_vp, _vp, _vp, _vp]),
     "nufft_plan1_exec": (_i, [_vp, _vp, _vp, _sz, _vp]),
     "nufft_plan1_exec_host": (_i, [_vp, _vp, _sz, _vp, _sz]),
+    "nufft_plan1_adjoint": (_i, [_vp, _vp, _vp, _vp]),
+    "nufft_plan1_adjoint_host": (_i, [_vp, _vp, _sz, _vp]),
+    "nufft_toeplitz_from_first_column": (_i, [_vp, _sz, _i, C.POINTER(_vp)]),
+    "nufft_toeplitz_from_normal": (_i, [_vp, C.POINTER(_vp)]),
+    "nufft_toeplitz_from_gram": (_i, [_vp, C.POINTER(_vp)]),
+    "nufft_toeplitz_destroy": (None, [_vp]),
+    "nufft_toeplitz_size": (_i, [_vp, C.POINTER(_sz)]),
+    "nufft_toeplitz_members": (_i, [_vp, _vp, _vp]),
+    "nufft_toeplitz_matvec": (_i, [_vp, _vp, _vp, _vp]),
+    "nufft_toeplitz_matvec_host": (_i, [_vp, _vp, _sz, _vp]),
+    "nufft_cg_toeplitz_host": (_i, [_vp, _vp, _sz, C.c_double, _sz, _vp, C.POINTER(CgReport), _vp, _sz]),
+    "nufft_inufft2_host": (_i, [_vp, _vp, _vp, _sz, C.c_double, _vp, C.POINTER(CgReport), _vp, _sz]),
+    "nufft_inufft2": (_i, [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(CgReport), _vp]),
+    "nufft_inufft1_host": (_i, [_vp, _vp, _vp, _sz, C.c_double, _vp, C.POINTER(CgReport), _vp, _sz]),
+    "nufft_default_cg_max_iter": (_sz, [_sz]),
     "nufft_plan3_create": (_i, [_vp, _vp, _sz, _sz, C.c_double, _i, C.POINTER(_vp)]),
     "nufft_plan3_destroy": (None, [_vp]),
     "nufft_plan3_info": (_i, [_vp, C.POINTER(PlanInfo)]),

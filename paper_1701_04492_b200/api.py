@@ -13,7 +13,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import PlanInfo, lib
+from ._lib import CgReport, PlanInfo, lib
 
 __all__ = [
     "InvalidArgument", "DomainError", "NufftError",
@@ -23,7 +23,9 @@ __all__ = [
     "normalize_samples", "grid_assign", "Plan2", "Plan1", "Plan3", "Plan2D",
     "plan_nufft2", "exec_nufft2", "exec_nufft2_adjoint", "plan_nufft1", "exec_nufft1",
     "plan_nufft3", "exec_nufft3", "plan_nufft2d2", "exec_nufft2d2", "exec_nufft2d2_impl",
-    "device_count",
+    "device_count", "ToeplitzOperator", "toeplitz_from_first_column", "toeplitz_from_normal",
+    "toeplitz_from_gram", "toeplitz_matvec", "cg_solve_toeplitz", "inufft2", "inufft1",
+    "default_cg_max_iter", "exec_nufft1_adjoint",
 ]
 
 
@@ -439,3 +441,117 @@ def exec_nufft2d2(plan: Plan2D, C2) -> np.ndarray:
 
 def exec_nufft2d2_impl(plan: Plan2D, C2, reuse_row_stage: bool) -> np.ndarray:
     return plan.execute(C2, reuse_row_stage)
+
+
+# ---------------------------------------------------------------- inverse (inverse.hpp)
+def exec_nufft1_adjoint(plan: Plan1, g) -> np.ndarray:
+    """F1~* g (transforms.hpp:294-300)."""
+    g = _c128(g)
+    out = np.empty_like(g)
+    _check(lib().nufft_plan1_adjoint_host(plan._h, _ptr(g), len(g), _ptr(out)))
+    return out
+
+
+class ToeplitzOperator:
+    """Hermitian Toeplitz operator in its 2N circulant embedding (inverse.hpp:22-27),
+    resident on the device; ``spectrum`` / ``firstColumn`` are host copies."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        n = C.c_size_t()
+        _check(lib().nufft_toeplitz_size(self._h, C.byref(n)))
+        self.n = n.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().nufft_toeplitz_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _members(self):
+        sp = np.zeros(2 * self.n, np.complex128)
+        fc = np.zeros(self.n, np.complex128)
+        _check(lib().nufft_toeplitz_members(self._h, _ptr(sp), _ptr(fc)))
+        return sp, fc
+
+    @property
+    def spectrum(self) -> np.ndarray:
+        return self._members()[0]
+
+    @property
+    def firstColumn(self) -> np.ndarray:  # noqa: N802 (reference member name)
+        return self._members()[1]
+
+    def matvec_device(self, v_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        _check(lib().nufft_toeplitz_matvec(self._h, v_ptr, out_ptr, stream or None))
+
+
+def toeplitz_from_first_column(column, device: int = -1) -> ToeplitzOperator:
+    col = _c128(column)
+    h = C.c_void_p()
+    _check(lib().nufft_toeplitz_from_first_column(_ptr(col), len(col), device, C.byref(h)))
+    return ToeplitzOperator(h)
+
+
+def toeplitz_from_normal(plan: Plan2) -> ToeplitzOperator:
+    h = C.c_void_p()
+    _check(lib().nufft_toeplitz_from_normal(plan._h, C.byref(h)))
+    return ToeplitzOperator(h)
+
+
+def toeplitz_from_gram(plan: Plan1) -> ToeplitzOperator:
+    h = C.c_void_p()
+    _check(lib().nufft_toeplitz_from_gram(plan._h, C.byref(h)))
+    return ToeplitzOperator(h)
+
+
+def toeplitz_matvec(op: ToeplitzOperator, v) -> np.ndarray:
+    v = _c128(v)
+    out = np.empty_like(v)
+    _check(lib().nufft_toeplitz_matvec_host(op._h, _ptr(v), len(v), _ptr(out)))
+    return out
+
+
+def default_cg_max_iter(n: int) -> int:
+    return int(lib().nufft_default_cg_max_iter(n))
+
+
+def _report(rep: CgReport, sol: np.ndarray, hist: np.ndarray) -> dict:
+    return {"solution": sol, "iterations": rep.iterations, "relativeResidual": rep.relative_residual,
+            "converged": bool(rep.converged), "residualHistory": hist[:rep.history_len].copy()}
+
+
+def cg_solve_toeplitz(op: ToeplitzOperator, rhs, tol: float, max_iter: int) -> dict:
+    """cg_solve (inverse.hpp:118-157) with the Toeplitz operator, on the device."""
+    rhs = _c128(rhs)
+    sol = np.empty_like(rhs)
+    hist = np.zeros(max(max_iter, 1))
+    rep = CgReport()
+    _check(lib().nufft_cg_toeplitz_host(op._h, _ptr(rhs), len(rhs), tol, max_iter, _ptr(sol), C.byref(rep),
+                                        _ptr(hist), len(hist)))
+    return _report(rep, sol, hist)
+
+
+def inufft2(plan: Plan2, f, tol: float, op: ToeplitzOperator | None = None) -> dict:
+    """Inverse type II (inverse.hpp:171-183): CG on the normal equations, on the device."""
+    f = _c128(f)
+    sol = np.empty_like(f)
+    hist = np.zeros(default_cg_max_iter(len(f)))
+    rep = CgReport()
+    _check(lib().nufft_inufft2_host(plan._h, op._h if op else None, _ptr(f), len(f), tol, _ptr(sol),
+                                    C.byref(rep), _ptr(hist), len(hist)))
+    return _report(rep, sol, hist)
+
+
+def inufft1(plan: Plan1, f, tol: float, op: ToeplitzOperator | None = None) -> dict:
+    """Inverse type I (inverse.hpp:187-200): CG on the Gram matrix, then c = F1~* y."""
+    f = _c128(f)
+    sol = np.empty_like(f)
+    hist = np.zeros(default_cg_max_iter(len(f)))
+    rep = CgReport()
+    _check(lib().nufft_inufft1_host(plan._h, op._h if op else None, _ptr(f), len(f), tol, _ptr(sol),
+                                    C.byref(rep), _ptr(hist), len(hist)))
+    return _report(rep, sol, hist)

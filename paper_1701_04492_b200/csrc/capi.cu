@@ -36,6 +36,9 @@ struct nufft_plan3 {
 struct nufft_plan2d {
     nb::Plan2DState st;
 };
+struct nufft_toeplitz {
+    nb::ToeplitzState st;
+};
 
 namespace {
 
@@ -378,7 +381,7 @@ static int plan2_create_impl(const double* x, bool on_dev, size_t n, double eps,
         cudaStream_t s = cudaStreamPerThread;
         nb::assign_samples(c.ax, x, on_dev, n, n, s);
         nb::finish_core(c, c.ax.gamma, s);
-        nb::build_bins(c, s);
+        if (!c.fused) nb::build_bins(c, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });
@@ -527,8 +530,9 @@ int nufft_plan1_create(const double* omega, size_t n, double epsilon, int device
         c.epsilon = epsilon;
         cudaStream_t s = cudaStreamPerThread;
         nb::assign_frequencies(c.ax, omega, false, n, false, s);
+        c.delta_from_freq = true;
         nb::finish_core(c, c.ax.gamma_raw, s);  // un-snapped gamma, transforms.hpp:282
-        nb::build_bins(c, s);
+        if (!c.fused) nb::build_bins(c, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });
@@ -570,6 +574,226 @@ int nufft_plan1_exec_host(const nufft_plan1* plan, const double* c, size_t len, 
 }
 
 // ------------------------------------------------------------ type III
+static void type1_adjoint_dev(const nb::CorePlan& p, const double2* gin, double2* out, cudaStream_t s) {
+    nb::DevBuf g(16 * p.n, s);
+    nb::conj_copy(gin, g.as<double2>(), p.n, s);
+    nb::exec_type2(p, g.as<double2>(), out, 1, 0, p.K, s);
+    nb::conj_copy(out, out, p.n, s);
+    nb::fft_count(p.n, p.K);
+}
+int nufft_plan1_adjoint(const nufft_plan1* plan, const double* g_dev, double* out_dev, void* stream) {
+    return guard([&] {
+        NB_CUDA(cudaSetDevice(plan->core.device));
+        type1_adjoint_dev(plan->core, reinterpret_cast<const double2*>(g_dev), reinterpret_cast<double2*>(out_dev),
+                          as_stream(stream));
+    });
+}
+int nufft_plan1_adjoint_host(const nufft_plan1* plan, const double* g, size_t len, double* out) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("nufft transpose: length mismatch");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(g, 2 * p.n, out, 2 * p.n, s, [&](double2* a, double2* b) { type1_adjoint_dev(p, a, b, s); });
+    });
+}
+
+// ------------------------------------------------------------ inverse
+static std::unique_ptr<nufft_toeplitz> toeplitz_make(int device, size_t n) {
+    auto op = std::make_unique<nufft_toeplitz>();
+    op->st.device = device;
+    op->st.n = n;
+    return op;
+}
+int nufft_toeplitz_from_first_column(const double* column, size_t n, int device, nufft_toeplitz** out) {
+    return guard([&] {
+        if (n == 0) nb::throw_invalid("toeplitz: empty first column");
+        const int dev = pick_device(device);
+        auto op = toeplitz_make(dev, n);
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf col(16 * n, s);
+        NB_CUDA(cudaMemcpyAsync(col.get(), column, 16 * n, cudaMemcpyHostToDevice, s));
+        nb::toeplitz_from_column(op->st, col.as<double2>(), s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = op.release();
+    });
+}
+int nufft_toeplitz_from_normal(const nufft_plan2* plan, nufft_toeplitz** out) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        auto op = toeplitz_make(p.device, p.n);
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf e0(16 * p.n, s), f(16 * p.n, s), col(16 * p.n, s);
+        NB_CUDA(cudaMemsetAsync(e0.get(), 0, 16 * p.n, s));
+        const double one = 1.0;
+        NB_CUDA(cudaMemcpyAsync(e0.get(), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+        nb::exec_type2(p, e0.as<double2>(), f.as<double2>(), 1, 0, p.K, s);  // F2~ e_0
+        nb::fft_count(p.n, p.K);
+        adjoint_dev(p, f.as<double2>(), col.as<double2>(), s);               // F2~* F2~ e_0
+        nb::toeplitz_from_column(op->st, col.as<double2>(), s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = op.release();
+    });
+}
+int nufft_toeplitz_from_gram(const nufft_plan1* plan, nufft_toeplitz** out) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        auto op = toeplitz_make(p.device, p.n);
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf e0(16 * p.n, s), g(16 * p.n, s), col(16 * p.n, s);
+        NB_CUDA(cudaMemsetAsync(e0.get(), 0, 16 * p.n, s));
+        const double one = 1.0;
+        NB_CUDA(cudaMemcpyAsync(e0.get(), &one, sizeof(double), cudaMemcpyHostToDevice, s));
+        type1_adjoint_dev(p, e0.as<double2>(), g.as<double2>(), s);    // F1~* e_0
+        nb::exec_transpose(p, g.as<double2>(), col.as<double2>(), 1, s);  // F1~ F1~* e_0
+        nb::fft_count(p.n, p.K);
+        nb::toeplitz_from_column(op->st, col.as<double2>(), s);
+        NB_CUDA(cudaStreamSynchronize(s));
+        *out = op.release();
+    });
+}
+void nufft_toeplitz_destroy(nufft_toeplitz* op) {
+    if (!op) return;
+    cudaSetDevice(op->st.device);
+    cudaDeviceSynchronize();
+    delete op;
+}
+int nufft_toeplitz_size(const nufft_toeplitz* op, size_t* n) {
+    return guard([&] { *n = op->st.n; });
+}
+int nufft_toeplitz_members(const nufft_toeplitz* op, double* spectrum, double* first_column) {
+    return guard([&] {
+        const nb::ToeplitzState& t = op->st;
+        NB_CUDA(cudaSetDevice(t.device));
+        cudaStream_t s = cudaStreamPerThread;
+        if (spectrum) {
+            std::vector<double> re(2 * t.n);
+            d2h(re.data(), t.spectrum, 2 * t.n, s);
+            NB_CUDA(cudaStreamSynchronize(s));
+            for (size_t j = 0; j < 2 * t.n; ++j) {
+                spectrum[2 * j] = re[j];
+                spectrum[2 * j + 1] = 0.0;
+            }
+        }
+        if (first_column) {
+            NB_CUDA(cudaMemcpyAsync(first_column, t.first_col.as<double2>(), 16 * t.n, cudaMemcpyDeviceToHost, s));
+            NB_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+int nufft_toeplitz_matvec(const nufft_toeplitz* op, const double* v_dev, double* out_dev, void* stream) {
+    return guard([&] {
+        NB_CUDA(cudaSetDevice(op->st.device));
+        nb::toeplitz_matvec(op->st, reinterpret_cast<const double2*>(v_dev), reinterpret_cast<double2*>(out_dev),
+                            as_stream(stream));
+    });
+}
+int nufft_toeplitz_matvec_host(const nufft_toeplitz* op, const double* v, size_t len, double* out) {
+    return guard([&] {
+        const nb::ToeplitzState& t = op->st;
+        if (len != t.n) nb::throw_invalid("toeplitz_matvec: length mismatch");
+        NB_CUDA(cudaSetDevice(t.device));
+        cudaStream_t s = cudaStreamPerThread;
+        host_roundtrip(v, 2 * t.n, out, 2 * t.n, s, [&](double2* a, double2* b) { nb::toeplitz_matvec(t, a, b, s); });
+    });
+}
+static void fill_report(const nb::CgResult& r, const std::vector<double>& hist, nufft_cg_report* rep,
+                        double* history, size_t cap) {
+    if (rep) {
+        rep->iterations = r.iterations;
+        rep->relative_residual = r.relative_residual;
+        rep->converged = r.converged ? 1 : 0;
+        rep->history_len = std::min(cap, hist.size());
+    }
+    if (history)
+        for (size_t i = 0; i < hist.size() && i < cap; ++i) history[i] = hist[i];
+}
+int nufft_cg_toeplitz_host(const nufft_toeplitz* op, const double* rhs, size_t len, double tol, size_t max_iter,
+                           double* solution, nufft_cg_report* report, double* history, size_t history_cap) {
+    return guard([&] {
+        if (!(tol > 0.0)) nb::throw_domain("cg_solve: tol must be positive");
+        const nb::ToeplitzState& t = op->st;
+        if (len != t.n) nb::throw_invalid("toeplitz_matvec: length mismatch");
+        NB_CUDA(cudaSetDevice(t.device));
+        cudaStream_t s = cudaStreamPerThread;
+        std::vector<double> hist;
+        nb::CgResult r;
+        host_roundtrip(rhs, 2 * t.n, solution, 2 * t.n, s, [&](double2* a, double2* b) {
+            r = nb::cg_solve_toeplitz(t, a, b, tol, max_iter, &hist, s);
+        });
+        fill_report(r, hist, report, history, history_cap);
+    });
+}
+static nb::CgResult inufft2_dev(const nufft_plan2* plan, const nufft_toeplitz* op, const double2* f, double tol,
+                                double2* sol, std::vector<double>* hist, cudaStream_t s) {
+    const nb::CorePlan& p = plan->core;
+    if (!(p.ax.gamma < 0.5)) nb::throw_domain("inufft2: gamma >= 1/2, samples may not be distinct");
+    if (!(tol > 0.0)) nb::throw_domain("cg_solve: tol must be positive");
+    std::unique_ptr<nufft_toeplitz> own;
+    if (!op) {
+        nufft_toeplitz* raw = nullptr;
+        if (nufft_toeplitz_from_normal(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, g_err);
+        own.reset(raw);
+        op = raw;
+    }
+    nb::DevBuf rhs(16 * p.n, s);
+    adjoint_dev(p, f, rhs.as<double2>(), s);
+    return nb::cg_solve_toeplitz(op->st, rhs.as<double2>(), sol, tol, nb::default_cg_max_iter(p.n), hist, s);
+}
+int nufft_inufft2_host(const nufft_plan2* plan, const nufft_toeplitz* op, const double* f, size_t len, double tol,
+                       double* solution, nufft_cg_report* report, double* history, size_t history_cap) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("inufft2: length mismatch");
+        if (!(p.ax.gamma < 0.5)) nb::throw_domain("inufft2: gamma >= 1/2, samples may not be distinct");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        std::vector<double> hist;
+        nb::CgResult r;
+        host_roundtrip(f, 2 * p.n, solution, 2 * p.n, s,
+                       [&](double2* a, double2* b) { r = inufft2_dev(plan, op, a, tol, b, &hist, s); });
+        fill_report(r, hist, report, history, history_cap);
+    });
+}
+int nufft_inufft2(const nufft_plan2* plan, const nufft_toeplitz* op, const double* f_dev, double tol,
+                  double* solution_dev, nufft_cg_report* report, void* stream) {
+    return guard([&] {
+        NB_CUDA(cudaSetDevice(plan->core.device));
+        const nb::CgResult r = inufft2_dev(plan, op, reinterpret_cast<const double2*>(f_dev), tol,
+                                           reinterpret_cast<double2*>(solution_dev), nullptr, as_stream(stream));
+        fill_report(r, {}, report, nullptr, 0);
+    });
+}
+int nufft_inufft1_host(const nufft_plan1* plan, const nufft_toeplitz* op, const double* f, size_t len, double tol,
+                       double* solution, nufft_cg_report* report, double* history, size_t history_cap) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("inufft1: length mismatch");
+        if (!(p.ax.gamma < 0.5)) nb::throw_domain("inufft1: gamma >= 1/2, frequencies may not be distinct");
+        if (!(tol > 0.0)) nb::throw_domain("cg_solve: tol must be positive");
+        NB_CUDA(cudaSetDevice(p.device));
+        std::unique_ptr<nufft_toeplitz> own;
+        if (!op) {
+            nufft_toeplitz* raw = nullptr;
+            if (nufft_toeplitz_from_gram(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, g_err);
+            own.reset(raw);
+            op = raw;
+        }
+        cudaStream_t s = cudaStreamPerThread;
+        std::vector<double> hist;
+        nb::CgResult r;
+        host_roundtrip(f, 2 * p.n, solution, 2 * p.n, s, [&](double2* a, double2* b) {
+            nb::DevBuf y(16 * p.n, s);
+            r = nb::cg_solve_toeplitz(op->st, a, y.as<double2>(), tol, nb::default_cg_max_iter(p.n), &hist, s);
+            type1_adjoint_dev(p, y.as<double2>(), b, s);  // c = F1~* y
+        });
+        fill_report(r, hist, report, history, history_cap);
+    });
+}
+size_t nufft_default_cg_max_iter(size_t n) { return nb::default_cg_max_iter(n); }
+
 int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, size_t n_omega,
                        double epsilon, int device, nufft_plan3** out) {
     return guard([&] {
@@ -587,6 +811,7 @@ int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, siz
         st.inner.n = n;
         st.inner.epsilon = epsilon;
         nb::assign_frequencies(st.inner.ax, omega, false, n, true, s);
+        st.inner.delta_from_freq = true;
         st.a.device = dev;
         st.a.n = n;
         st.a.epsilon = epsilon;
@@ -610,7 +835,7 @@ int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, siz
         st.kc = st.btrivial ? st.a.K : 2 * st.a.K;
         // inner type-I plan on omega (transforms.hpp:378)
         nb::finish_core(st.inner, st.inner.ax.gamma_raw, s);
-        nb::build_bins(st.inner, s);
+        if (!st.inner.fused) nb::build_bins(st.inner, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });

@@ -302,6 +302,8 @@ struct Pass2Params {
     int log_n1, log_n2;
     int r0, r1;
     const double* xs;
+    const double* ds;        // type-I cores: delta and key in bucket order (xs would round omega/N)
+    const unsigned* skey;
     const int* perm;
     const int* rowoff;
     unsigned long long* trace;  // diagnostics: per-iteration clock64 stamps of CTA 0 (nullptr = off)
@@ -381,6 +383,25 @@ __device__ __forceinline__ void horner_step(double2 (&acc)[Q], int r, int deg, c
     }
 }
 
+// t2 and h = -pi delta / 2 of sorted sample idx: recomputed from x exactly
+// as the reference does (transforms.hpp:60-64,84-86), or — for type-I cores,
+// whose delta = omega - round(omega) is not recoverable from omega/N
+// (transforms.hpp:262-272) — read from the plan's sorted copies.
+__device__ __forceinline__ void sample_geom(const Pass2Params& p, int idx, int& t2, double& h) {
+    if (p.ds) {
+        h = half_phase(p.ds[idx]);
+        t2 = (int)(p.skey[idx] & ((1u << p.log_n2) - 1u));
+        return;
+    }
+    const double dn = (double)p.n;
+    const double x = p.xs[idx];
+    const double pr = __dmul_rn(dn, x);
+    const long long sj = (long long)round(pr);
+    const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+    t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
+    h = half_phase(d);
+}
+
 // sample setup: recompute s, t, delta exactly (transforms.hpp:60-64,84-86) from sorted x
 template <int Q, int G>
 __device__ __forceinline__ void load_samples(const Pass2Params& p, int cb, int cnt, int tid,
@@ -391,13 +412,11 @@ __device__ __forceinline__ void load_samples(const Pass2Params& p, int cb, int c
         acc[q] = make_double2(0.0, 0.0);
         const int i = tid + q * G;
         if (i < cnt) {
-            const double x = p.xs[cb + i];
-            const double pr = __dmul_rn(dn, x);
-            const long long sj = (long long)round(pr);
-            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
-            const long long t = sj & (p.n - 1);
-            st2[i] = (int)(t >> p.log_n1);
-            sh[i] = half_phase(d);
+            int t2;
+            double h;
+            sample_geom(p, cb + i, t2, h);
+            st2[i] = t2;
+            sh[i] = h;
         } else {  // idle slot: harmless inputs for the unpredicated Horner step
             st2[i] = 0;
             sh[i] = 0.0;
@@ -768,14 +787,7 @@ __global__ void __launch_bounds__(TmShape<L2>::ALL, 1)
                         const int i = tid + q * S;
                         h[u] = 0.0;
                         t2[u] = 0;
-                        if (i < cnt) {
-                            const double x = p.xs[cb + i];
-                            const double pr = __dmul_rn(dn, x);
-                            const long long sj = (long long)round(pr);
-                            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
-                            t2[u] = (int)((sj & (p.n - 1)) >> p.log_n1);
-                            h[u] = half_phase(d);
-                        }
+                        if (i < cnt) sample_geom(p, cb + i, t2[u], h[u]);
                     }
                     tm_st4(tcol + 8 * k, lo32(h[0]), hi32(h[0]), lo32(h[1]), hi32(h[1]));
                     tm_st4(tcol + 8 * k + 4, lo32(h[2]), hi32(h[2]), lo32(h[3]), hi32(h[3]));
@@ -959,14 +971,7 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                         const int i = tid + (4 * k + u) * S;
                         double h = 0.0;
                         int t2 = 0;
-                        if (i < cnt) {
-                            const double x = p.xs[cb + i];
-                            const double pr = __dmul_rn(dn, x);
-                            const long long sj = (long long)round(pr);
-                            const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
-                            t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
-                            h = half_phase(d);
-                        }
+                        if (i < cnt) sample_geom(p, cb + i, t2, h);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
                         hv[2 * u] = lo32(h);
@@ -1211,6 +1216,8 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.r0 = r0;
     p.r1 = r1;
     p.xs = pl.bk.xs.as<double>();
+    p.ds = pl.delta_from_freq ? pl.bk.ds.as<double>() : nullptr;
+    p.skey = pl.delta_from_freq ? pl.bk.skey.as<unsigned>() : nullptr;
     p.perm = pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];

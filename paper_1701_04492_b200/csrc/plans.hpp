@@ -56,6 +56,7 @@ struct CorePlan {
     bool fused = false;         // power-of-two fused two-pass path
     Buckets bk;
     bool have_bins = false;     // bin_off / sort_perm built (transpose core)
+    bool delta_from_freq = false;  // type-I axis: delta = omega - round(omega), not N x - s
 };
 
 struct Plan3State {
@@ -116,6 +117,24 @@ void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_
 void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s);
+
+// ---- inverse (inverse.cu): Toeplitz operator in its 2N circulant embedding
+struct ToeplitzState {
+    int device = 0;
+    size_t n = 0;
+    DevArray spectrum;   // 2n doubles: Re(FFT_2n(symbol)) (inverse.hpp:37-50)
+    DevArray first_col;  // n complex
+};
+struct CgResult {
+    size_t iterations = 0;
+    double relative_residual = 0.0;
+    bool converged = false;
+};
+void toeplitz_from_column(ToeplitzState& op, const double2* col_dev, cudaStream_t s);
+void toeplitz_matvec(const ToeplitzState& op, const double2* v, double2* out, cudaStream_t s);
+CgResult cg_solve_toeplitz(const ToeplitzState& op, const double2* rhs, double2* x, double tol,
+                           size_t max_iter, std::vector<double>* history, cudaStream_t s);
+size_t default_cg_max_iter(size_t n);
 
 bool fused_2d_eligible(size_t m, size_t n, size_t count);
 void build_2d_fused(Plan2DState& st, cudaStream_t s);

@@ -16,7 +16,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "oracle", "_ref")
-SUITES = ["fft", "special", "lowrank", "oracle", "transforms", "transform2d"]
+SUITES = ["fft", "special", "lowrank", "oracle", "transforms", "transform2d", "inverse"]
 
 
 def _bin(name):
