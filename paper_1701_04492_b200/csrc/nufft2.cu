@@ -949,14 +949,18 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                                      "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
                     }
                     const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
+                    const bool tr = row == blockIdx.x && cb == beg;
+                    if (tr) NB_TRACE(8 * i + 0);
                     double2 v[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
                     if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
+                    if (tr) NB_TRACE(8 * i + 1);
                     if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                     gsync();  // last-stage reads of buf done
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    if (tr) NB_TRACE(8 * i + 2);
                     nbar_arrive(BAR_FULL + b, PAIR);
                 }
             } else {
@@ -1009,6 +1013,7 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                     const int b = i % 3;
                     const double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, PAIR);
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 4);
                     const double* a = kBes + r * kSeriesTerms;
                     const int deg = p.deg[r];
                     (void)a;
@@ -1052,6 +1057,7 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                     }
                     // release b only to a later step (an EMPTY arrival nobody waits
                     // for would pair with the next use of the barrier)
+                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 5);
                     if (i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
                 }
                 tm_wait_st();

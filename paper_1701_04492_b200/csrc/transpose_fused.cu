@@ -30,6 +30,7 @@
 #include "bessel.cuh"
 #include "fft_block.cuh"
 #include "plans.hpp"
+#include "tmem.cuh"
 
 namespace nb {
 
@@ -280,6 +281,133 @@ __global__ void __launch_bounds__(L1 / 16, 1)
     }
 }
 
+// Two-worker pass B (L1 = 2048, 4096): two independent column workers per CTA
+// (columns 2*blockIdx + g, stride 2*gridDim) for twice the warps in flight;
+// the accumulator and the Chebyshev state of each thread's 16 points live in
+// tensor memory (tmem.cuh: 128 columns per thread, [acc re/im lo/hi x 16]
+// [T_{r-1}, T_r lo/hi x 16]) instead of 128 registers, and each worker
+// exchanges through one padded buffer of its own (as k2_pass1_tm, nufft2.cu).
+template <int L1, bool UNIFORM>
+__global__ void __launch_bounds__(2 * (L1 / 16), 1)
+    k1_passB_tm(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p) {
+    constexpr int G = L1 / 16;
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x / G;
+    const int tid = threadIdx.x - grp * G;
+    double2* buf = smem + grp * padded_len(L1);
+    double2* step = smem + 2 * padded_len(L1) + grp * 16;
+    double2* tw = smem + 2 * padded_len(L1) + 32;
+    twiddle_table_build<L1>(tw, threadIdx.x, 2 * G);
+    Twiddles<L1> T;
+    twiddle_init<L1>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 128);
+    const unsigned tc_a = tcol, tc_s = tcol + 64;
+    const int bar = 1 + grp;
+    auto gsync = [bar] {
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory");
+    };
+    const long long n2 = 1ll << p.log_n2;
+    const long long N = p.n;
+    for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
+        gsync();  // previous column's readers of step are done
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
+        const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
+        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // acc = 0, state (T_{r0-1}, T_r0)
+            unsigned av[16], sv[16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double ts = two_s0 + 0.25 * (4 * j + u);
+                double tprev = 1.0, tcur = 0.5 * ts;
+                for (int r = 1; r < p.r0; ++r) {
+                    const double tn = __fma_rn(ts, tcur, -tprev);
+                    tprev = tcur;
+                    tcur = tn;
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
+                sv[4 * u] = lo32(tprev);
+                sv[4 * u + 1] = hi32(tprev);
+                sv[4 * u + 2] = lo32(tcur);
+                sv[4 * u + 3] = hi32(tcur);
+            }
+            tm_st16(tc_a + 16 * j, av);
+            if constexpr (!UNIFORM) tm_st16(tc_s + 16 * j, sv);
+        }
+        tm_wait_st();
+        gsync();  // step visible
+        for (int r = p.r0; r < p.r1; ++r) {
+            const double2* col = Z + (long long)(r - p.r0) * N + k2;
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const long long t1 = tid + q * G;
+                v[q] = cmul(__ldcg(col + (t1 << p.log_n2)), cmul(base, step[q]));
+            }
+            gsync();  // previous term's last-stage reads of buf are done
+            block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                unsigned av[16], sv[16];
+                tm_ld16(tc_a + 16 * j, av);
+                if constexpr (!UNIFORM) tm_ld16(tc_s + 16 * j, sv);
+                tm_wait_ld();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = 4 * j + u;
+                    double2 a = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+                    if constexpr (UNIFORM) {
+                        a = cadd(a, v[q]);
+                    } else {
+                        const double tprev = mk64(sv[4 * u], sv[4 * u + 1]);
+                        const double tcur = mk64(sv[4 * u + 2], sv[4 * u + 3]);
+                        const double vr = (r == 0) ? 0.5 : tcur;
+                        a.x = __fma_rn(vr, v[q].x, a.x);
+                        a.y = __fma_rn(vr, v[q].y, a.y);
+                        if (r > 0) {
+                            const double tn = __fma_rn(two_s0 + 0.25 * q, tcur, -tprev);
+                            sv[4 * u] = sv[4 * u + 2];
+                            sv[4 * u + 1] = sv[4 * u + 3];
+                            sv[4 * u + 2] = lo32(tn);
+                            sv[4 * u + 3] = hi32(tn);
+                        }
+                    }
+                    av[4 * u] = lo32(a.x);
+                    av[4 * u + 1] = hi32(a.x);
+                    av[4 * u + 2] = lo32(a.y);
+                    av[4 * u + 3] = hi32(a.y);
+                }
+                tm_st16(tc_a + 16 * j, av);
+                if constexpr (!UNIFORM) {
+                    if (r > 0) tm_st16(tc_s + 16 * j, sv);
+                }
+            }
+        }
+        tm_wait_st();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            unsigned av[16];
+            tm_ld16(tc_a + 16 * j, av);
+            tm_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long k1 = tid + (4 * j + u) * G;
+                f[(k1 << p.log_n2) + k2] =
+                    make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+            }
+        }
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
 // N1 == 1: f[k] = sum_r v_r(k) Z_r[k]
 __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ f, long long N,
                            int r0, int r1, int uniform) {
@@ -349,6 +477,17 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
 template <int L1>
 void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
+    if constexpr (L1 >= 2048) {
+        constexpr size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
+        PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+        auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
+        set_smem(fn, SMT);
+        const long long n2 = 1ll << pl.bk.log_n2;
+        const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
+        fn<<<grid, 2 * (L1 / 16), SMT, s>>>(Z, f, p);
+        NB_LAUNCH();
+        return;
+    }
     constexpr size_t SM = sizeof(double2) * (2 * padded_len(L1) + 16 + FftShapeX<L1>::TW_LEN);
     PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
     auto fn = pl.uniform ? k1_passB<L1, true> : k1_passB<L1, false>;
