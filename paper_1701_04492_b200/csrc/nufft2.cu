@@ -315,43 +315,6 @@ struct Pass2Params {
         if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[(slot)] = clock64();           \
     } while (0)
 
-// g_r(w) for C samples at once, degree D fixed at compile time: one
-// (uniform, constant-bank) coefficient load feeds C independent FMAs.
-template <int C, int D>
-__device__ __forceinline__ void series_fixed(double (&g)[C], const double (&w)[C], const double* a) {
-#pragma unroll
-    for (int c = 0; c < C; ++c) g[c] = a[D];
-#pragma unroll
-    for (int m = D - 1; m >= 0; --m) {
-        const double am = a[m];
-#pragma unroll
-        for (int c = 0; c < C; ++c) g[c] = __fma_rn(g[c], w[c], am);
-    }
-}
-
-// runtime degree (warp-uniform) -> unrolled straight-line Horner
-template <int C>
-__device__ __forceinline__ void series_deg(double (&g)[C], const double (&w)[C], const double* a, int deg) {
-    switch (deg) {
-        case 0: series_fixed<C, 0>(g, w, a); break;
-        case 1: series_fixed<C, 1>(g, w, a); break;
-        case 2: series_fixed<C, 2>(g, w, a); break;
-        case 3: series_fixed<C, 3>(g, w, a); break;
-        case 4: series_fixed<C, 4>(g, w, a); break;
-        case 5: series_fixed<C, 5>(g, w, a); break;
-        case 6: series_fixed<C, 6>(g, w, a); break;
-        case 7: series_fixed<C, 7>(g, w, a); break;
-        case 8: series_fixed<C, 8>(g, w, a); break;
-        case 9: series_fixed<C, 9>(g, w, a); break;
-        case 10: series_fixed<C, 10>(g, w, a); break;
-        case 11: series_fixed<C, 11>(g, w, a); break;
-        case 12: series_fixed<C, 12>(g, w, a); break;
-        case 13: series_fixed<C, 13>(g, w, a); break;
-        case 14: series_fixed<C, 14>(g, w, a); break;
-        default: series_fixed<C, kSeriesTerms - 1>(g, w, a); break;
-    }
-}
-
 // One Horner step in r for the thread's samples: acc <- acc*(i h) + g_r(h^2) X_r[t2].
 // Samples go in chunks of C with a straight-line series per chunk; slots past
 // the chunk's sample count hold h = 0, t2 = 0 (load_samples) so no lane

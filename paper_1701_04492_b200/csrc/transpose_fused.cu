@@ -202,6 +202,199 @@ __global__ void __launch_bounds__(L2 / 16, 1)
     }
 }
 
+// Two-worker pass A (L2 = 2048, 4096): each CTA runs two independent row
+// workers (rows 2*blockIdx + g, stride 2*gridDim), so one worker's term/bin
+// phases overlap the other's FFT.  The per-sample state moves from shared
+// memory to tensor memory (tmem.cuh): per owned sample Q_j = h_j^r G_j
+// (4 columns, advanced by one multiply by h_j per term) and h_j (2 columns),
+// 17 samples x 6 = 102 columns per thread; each worker keeps one padded
+// buffer (terms, then FFT exchange) and its bin table in shared memory.
+template <int L2>
+struct PassATmShape {
+    static constexpr int G = L2 / 16;
+    static constexpr int QA = 17;
+    static constexpr int CAP = QA * G;
+    static constexpr int COL_Q = 0, COL_H = 4 * QA;  // 68 + 34 = 102 columns
+    static constexpr size_t SMEM = sizeof(double2) * (2 * padded_len(L2) + FftShapeX<L2>::TW_LEN) +
+                                   2 * sizeof(unsigned) * L2;
+    static_assert(SMEM <= kSmemLimit, "pass A (two workers) shared memory");
+    static_assert((2 * G / 32 + 3) / 4 * 6 * QA <= 512, "TMEM columns");
+};
+
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(2 * (L2 / 16), 1)
+    k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p) {
+    using S = PassATmShape<L2>;
+    constexpr int G = S::G;
+    constexpr int QA = S::QA;
+    constexpr int CAP = S::CAP;
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x / G;
+    const int tid = threadIdx.x - grp * G;
+    double2* buf = smem + grp * padded_len(L2);
+    double2* tw = smem + 2 * padded_len(L2);
+    unsigned* bo = reinterpret_cast<unsigned*>(tw + FftShapeX<L2>::TW_LEN) + grp * L2;
+    unsigned short* bo16 = reinterpret_cast<unsigned short*>(bo);
+    twiddle_table_build<L2>(tw, threadIdx.x, 2 * G);
+    Twiddles<L2> T;
+    twiddle_init<L2>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 6 * QA);
+    const int bar = 1 + grp;
+    auto gsync = [bar] { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory"); };
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const unsigned mask = (1u << p.log_n2) - 1u;
+    for (long long row = 2ll * blockIdx.x + grp; row < n1; row += 2ll * gridDim.x) {
+        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
+        if (beg == end) {  // empty row: Z_r[row][:] = 0
+            for (int r = p.r0; r < p.r1; ++r) {
+                double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) out[tid + q * G] = make_double2(0.0, 0.0);
+            }
+            continue;
+        }
+        for (int cb = beg, chunk = 0; cb < end; cb += CAP, ++chunk) {
+            const int cnt = min(CAP, end - cb);
+            gsync();  // previous chunk's readers of bo / buf are done
+            for (int i = tid; i < L2; i += G) bo[i] = 0u;
+            gsync();
+            for (int i = tid; i < cnt; i += G) {
+                const unsigned t2 = p.skey[cb + i] & mask;
+                if (i == 0 || (p.skey[cb + i - 1] & mask) != t2) bo16[2 * t2] = (unsigned short)i;
+                if (i == cnt - 1 || (p.skey[cb + i + 1] & mask) != t2) bo16[2 * t2 + 1] = (unsigned short)(i + 1);
+            }
+            // owned samples i = tid + u G: Q = h^r0 G_j (G_j = 2 exp(2ih) g_j), h
+#pragma unroll
+            for (int k = 0; k < (QA + 3) / 4; ++k) {
+                unsigned qv[16], hv[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int uu = 4 * k + u;
+                    const int i = tid + uu * G;
+                    double2 Gj = make_double2(0.0, 0.0);
+                    double h = 0.0;
+                    if (uu < QA && i < cnt) {
+                        Gj = __ldg(g + p.perm[cb + i]);
+                        if constexpr (!UNIFORM) {
+                            h = half_phase(p.ds[cb + i]);
+                            double sn, cs;
+                            sincos(2.0 * h, &sn, &cs);
+                            Gj = cmul(make_double2(2.0 * cs, 2.0 * sn), Gj);
+                            for (int r = 0; r < p.r0; ++r) Gj = cscale(Gj, h);
+                        }
+                    }
+                    qv[4 * u] = lo32(Gj.x);
+                    qv[4 * u + 1] = hi32(Gj.x);
+                    qv[4 * u + 2] = lo32(Gj.y);
+                    qv[4 * u + 3] = hi32(Gj.y);
+                    hv[2 * u] = lo32(h);
+                    hv[2 * u + 1] = hi32(h);
+                }
+                if (4 * k + 4 <= QA) {
+                    tm_st16(tcol + S::COL_Q + 16 * k, qv);
+                    tm_st8(tcol + S::COL_H + 8 * k, hv);
+                } else {  // QA % 4 == 1: the last sample alone
+                    tm_st4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                    unsigned h2[8] = {hv[0], hv[1], 0, 0, 0, 0, 0, 0};
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(tcol + S::COL_H + 8 * k),
+                                 "r"(h2[0]), "r"(h2[1])
+                                 : "memory");
+                }
+            }
+            tm_wait_st();
+            for (int r = p.r0; r < p.r1; ++r) {
+                gsync();  // previous term's last-stage reads of buf are done
+                // term phase: buf[i] = g_r(h_i^2) Q_i, then Q_i <- h_i Q_i
+                const double* a = kBes + r * kSeriesTerms;
+                const int deg = p.deg[r];
+#pragma unroll
+                for (int k = 0; k < (QA + 3) / 4; ++k) {
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    const bool full = 4 * k + 4 <= QA;
+                    unsigned qv[16], hv[8];
+                    if (full) {
+                        tm_ld16(tcol + S::COL_Q + 16 * k, qv);
+                        tm_ld8(tcol + S::COL_H + 8 * k, hv);
+                    } else {
+                        tm_ld4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                                     : "=r"(hv[0]), "=r"(hv[1])
+                                     : "r"(tcol + S::COL_H + 8 * k)
+                                     : "memory");
+#pragma unroll
+                        for (int c = 4; c < 16; ++c) qv[c] = 0u;
+#pragma unroll
+                        for (int c = 2; c < 8; ++c) hv[c] = 0u;
+                    }
+                    tm_wait_ld();
+                    double h[4], w[4], gr[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        h[u] = mk64(hv[2 * u], hv[2 * u + 1]);
+                        w[u] = h[u] * h[u];
+                    }
+                    if constexpr (UNIFORM) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) gr[u] = 1.0;
+                    } else {
+                        series_deg<4>(gr, w, a, deg);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int uu = 4 * k + u;
+                        if (uu >= QA) break;
+                        const double2 Qv =
+                            make_double2(mk64(qv[4 * u], qv[4 * u + 1]), mk64(qv[4 * u + 2], qv[4 * u + 3]));
+                        buf[tid + uu * G] = cscale(Qv, gr[u]);
+                        const double2 Qn = UNIFORM ? Qv : cscale(Qv, h[u]);
+                        qv[4 * u] = lo32(Qn.x);
+                        qv[4 * u + 1] = hi32(Qn.x);
+                        qv[4 * u + 2] = lo32(Qn.y);
+                        qv[4 * u + 3] = hi32(Qn.y);
+                    }
+                    if constexpr (!UNIFORM) {
+                        if (full) tm_st16(tcol + S::COL_Q + 16 * k, qv);
+                        else tm_st4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                    }
+                }
+                gsync();  // terms visible
+                double2 v[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const unsigned rb = bo[tid + q * G];
+                    const int i0 = rb & 0xffffu, i1 = rb >> 16;
+                    double2 acc = make_double2(0.0, 0.0);
+                    if (i0 < i1) {
+                        acc = buf[i0];
+                        for (int i = i0 + 1; i < i1; ++i) acc = cadd(acc, buf[i]);
+                    }
+                    v[q] = acc;
+                }
+                gsync();  // terms read before stage 1 reuses buf
+                block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double2 z = UNIFORM ? v[q] : rot_ipow(v[q], r);
+                    const int k2 = tid + q * G;
+                    out[k2] = chunk == 0 ? z : cadd(out[k2], z);
+                }
+            }
+            tm_wait_st();
+        }
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
 // pass B: column k2 of every Z_r, inter-pass twiddle, N1-point FFT, v_r accumulate
 template <int L1, bool UNIFORM>
 __global__ void __launch_bounds__(L1 / 16, 1)
@@ -466,6 +659,16 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
     p.perm = pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
+    if constexpr (L2 == 4096) {  // at 2048 two single-worker CTAs per SM are as good
+        constexpr size_t SMT = PassATmShape<L2>::SMEM;
+        auto fnt = pl.uniform ? k1_passA_tm<L2, true> : k1_passA_tm<L2, false>;
+        set_smem(fnt, SMT);
+        const long long rows = 1ll << pl.bk.log_n1;
+        const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
+        fnt<<<gridt, 2 * (L2 / 16), SMT, s>>>(g, Z, p);
+        NB_LAUNCH();
+        return;
+    }
     auto fn = pl.uniform ? k1_passA<L2, true> : k1_passA<L2, false>;
     set_smem(fn, SM);
     const long long n1 = 1ll << pl.bk.log_n1;
