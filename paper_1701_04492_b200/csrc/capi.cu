@@ -6,6 +6,7 @@
 //   plan_nufft3 :321-380, plan_nufft2d2 transform2d.hpp:65-100,
 //   exec length checks :171, :208, :384, transform2d.hpp:109-110.
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -381,7 +382,7 @@ static int plan2_create_impl(const double* x, bool on_dev, size_t n, double eps,
         cudaStream_t s = cudaStreamPerThread;
         nb::assign_samples(c.ax, x, on_dev, n, n, s);
         nb::finish_core(c, c.ax.gamma, s);
-        if (!c.fused) nb::build_bins(c, s);
+        if (!c.fused || getenv("NUFFT_PLAN_BINS")) nb::build_bins(c, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });

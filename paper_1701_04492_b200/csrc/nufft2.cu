@@ -867,7 +867,7 @@ struct G2Shape {
     static_assert(SMEM <= 227 * 1024, "pass 2 (two groups) shared memory");
 };
 
-template <int L2, bool UNIFORM>
+template <int L2, bool UNIFORM, bool DSRC>
 __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
     k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
     using W = G2Shape<L2>;
@@ -912,18 +912,14 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                                      "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
                     }
                     const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
-                    const bool tr = row == blockIdx.x && cb == beg;
-                    if (tr) NB_TRACE(8 * i + 0);
                     double2 v[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
                     if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
-                    if (tr) NB_TRACE(8 * i + 1);
                     if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                     gsync();  // last-stage reads of buf done
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
-                    if (tr) NB_TRACE(8 * i + 2);
                     nbar_arrive(BAR_FULL + b, PAIR);
                 }
             } else {
@@ -938,7 +934,19 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                         const int i = tid + (4 * k + u) * S;
                         double h = 0.0;
                         int t2 = 0;
-                        if (i < cnt) sample_geom(p, cb + i, t2, h);
+                        if (i < cnt) {
+                            if constexpr (DSRC) {  // type-I core: stored delta and key
+                                h = half_phase(p.ds[cb + i]);
+                                t2 = (int)(p.skey[cb + i] & ((1u << p.log_n2) - 1u));
+                            } else {
+                                const double x = p.xs[cb + i];
+                                const double pr = __dmul_rn(dn, x);
+                                const long long sj = (long long)round(pr);
+                                const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                                t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
+                                h = half_phase(d);
+                            }
+                        }
 #pragma unroll
                         for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
                         hv[2 * u] = lo32(h);
@@ -976,7 +984,6 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                     const int b = i % 3;
                     const double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, PAIR);
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 4);
                     const double* a = kBes + r * kSeriesTerms;
                     const int deg = p.deg[r];
                     (void)a;
@@ -1020,7 +1027,6 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                     }
                     // release b only to a later step (an EMPTY arrival nobody waits
                     // for would pair with the next use of the barrier)
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 5);
                     if (i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
                 }
                 tm_wait_st();
@@ -1156,7 +1162,7 @@ template <int L2, bool UNIFORM>
 void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
     constexpr size_t SM = G2Shape<L2>::SMEM;
     constexpr int threads = G2Shape<L2>::ALL;
-    auto fn = k2_pass2_g2<L2, UNIFORM>;
+    auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true> : k2_pass2_g2<L2, UNIFORM, false>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);
