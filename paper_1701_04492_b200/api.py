@@ -25,7 +25,7 @@ __all__ = [
     "plan_nufft3", "exec_nufft3", "plan_nufft2d2", "exec_nufft2d2", "exec_nufft2d2_impl",
     "device_count", "ToeplitzOperator", "toeplitz_from_first_column", "toeplitz_from_normal",
     "toeplitz_from_gram", "toeplitz_matvec", "cg_solve_toeplitz", "inufft2", "inufft1",
-    "default_cg_max_iter", "exec_nufft1_adjoint",
+    "default_cg_max_iter", "exec_nufft1_adjoint", "inufft2_device",
 ]
 
 
@@ -544,6 +544,16 @@ def inufft2(plan: Plan2, f, tol: float, op: ToeplitzOperator | None = None) -> d
     _check(lib().nufft_inufft2_host(plan._h, op._h if op else None, _ptr(f), len(f), tol, _ptr(sol),
                                     C.byref(rep), _ptr(hist), len(hist)))
     return _report(rep, sol, hist)
+
+
+def inufft2_device(plan: Plan2, f_ptr: int, tol: float, sol_ptr: int, op: ToeplitzOperator | None = None,
+                   stream: int = 0) -> dict:
+    """Device-pointer inufft2 (nufft_inufft2): f and the solution stay in HBM."""
+    rep = CgReport()
+    _check(lib().nufft_inufft2(plan._h, op._h if op else None, f_ptr, tol, sol_ptr, C.byref(rep),
+                               stream or None))
+    return {"iterations": rep.iterations, "relativeResidual": rep.relative_residual,
+            "converged": bool(rep.converged)}
 
 
 def inufft1(plan: Plan1, f, tol: float, op: ToeplitzOperator | None = None) -> dict:
