@@ -185,6 +185,18 @@ int nufft_inufft1_host(const nufft_plan1* plan, const nufft_toeplitz* op, const 
                        size_t history_cap);
 size_t nufft_default_cg_max_iter(size_t n); /* detail::default_cg_max_iter inverse.hpp:161-164 */
 
+/* ------------------------------------------------------------- direct sums (oracle.hpp) */
+/* nudft_direct oracle.hpp:70-86 on the device: f_j = sum_k c_k exp(-2 pi i x_j w_k) for
+ * j < nx (the reference requires nx == n; a subset of outputs is allowed here),
+ * exact product split + double-double reduction of the phase, Neumaier sums in
+ * ascending k.  nudft2d_direct :90-107 (C row-major m x n, rows <-> y). */
+int nufft_nudft_direct_host(const double* x, size_t nx, const double* omega, const double* c, size_t n,
+                            double* f, int device);
+int nufft_nudft_direct(const double* x_dev, size_t nx, const double* omega_dev, const double* c_dev,
+                       size_t n, double* f_dev, void* stream);
+int nufft_nudft2d_direct_host(const double* x, const double* y, size_t count, const double* C, size_t m,
+                              size_t n, double* f, int device);
+
 /* ------------------------------------------------------------- type III */
 int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, size_t n_omega,
                        double epsilon, int device, nufft_plan3** out);   /* transforms.hpp:321-380 */

@@ -85,6 +85,9 @@ _SIGS = {
     "nufft_inufft2": (_i, [_vp, _vp, _vp, C.c_double, _vp, C.POINTER(CgReport), _vp]),
     "nufft_inufft1_host": (_i, [_vp, _vp, _vp, _sz, C.c_double, _vp, C.POINTER(CgReport), _vp, _sz]),
     "nufft_default_cg_max_iter": (_sz, [_sz]),
+    "nufft_nudft_direct_host": (_i, [_vp, _sz, _vp, _vp, _sz, _vp, _i]),
+    "nufft_nudft_direct": (_i, [_vp, _sz, _vp, _vp, _sz, _vp, _vp]),
+    "nufft_nudft2d_direct_host": (_i, [_vp, _vp, _sz, _vp, _sz, _sz, _vp, _i]),
     "nufft_plan3_create": (_i, [_vp, _vp, _sz, _sz, C.c_double, _i, C.POINTER(_vp)]),
     "nufft_plan3_destroy": (None, [_vp]),
     "nufft_plan3_info": (_i, [_vp, C.POINTER(PlanInfo)]),

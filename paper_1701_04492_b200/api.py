@@ -25,7 +25,7 @@ __all__ = [
     "plan_nufft3", "exec_nufft3", "plan_nufft2d2", "exec_nufft2d2", "exec_nufft2d2_impl",
     "device_count", "ToeplitzOperator", "toeplitz_from_first_column", "toeplitz_from_normal",
     "toeplitz_from_gram", "toeplitz_matvec", "cg_solve_toeplitz", "inufft2", "inufft1",
-    "default_cg_max_iter", "exec_nufft1_adjoint", "inufft2_device",
+    "default_cg_max_iter", "exec_nufft1_adjoint", "inufft2_device", "nudft_direct", "nudft2d_direct",
 ]
 
 
@@ -565,3 +565,25 @@ def inufft1(plan: Plan1, f, tol: float, op: ToeplitzOperator | None = None) -> d
     _check(lib().nufft_inufft1_host(plan._h, op._h if op else None, _ptr(f), len(f), tol, _ptr(sol),
                                     C.byref(rep), _ptr(hist), len(hist)))
     return _report(rep, sol, hist)
+
+
+# ---------------------------------------------------------------- direct sums (oracle.hpp:70-107)
+def nudft_direct(x, omega, c, device: int = -1) -> np.ndarray:
+    """f_j = sum_k c_k exp(-2 pi i x_j w_k) on the GPU (exact phase split, Neumaier sums).
+    Unlike the reference, len(x) may differ from len(omega) == len(c) (output subsets)."""
+    x, w, c = _f64(x), _f64(omega), _c128(c)
+    if len(w) != len(c):
+        raise InvalidArgument("nudft_direct: length mismatch")
+    f = np.empty(len(x), np.complex128)
+    _check(lib().nufft_nudft_direct_host(_ptr(x), len(x), _ptr(w), _ptr(c), len(c), _ptr(f), device))
+    return f
+
+
+def nudft2d_direct(x, y, C2, device: int = -1) -> np.ndarray:
+    x, y, C2 = _f64(x), _f64(y), _c128(C2)
+    if len(x) != len(y):
+        raise InvalidArgument("nudft2d_direct: sample length mismatch")
+    f = np.empty(len(x), np.complex128)
+    _check(lib().nufft_nudft2d_direct_host(_ptr(x), _ptr(y), len(x), _ptr(C2), C2.shape[0], C2.shape[1],
+                                           _ptr(f), device))
+    return f

@@ -795,6 +795,46 @@ int nufft_inufft1_host(const nufft_plan1* plan, const nufft_toeplitz* op, const 
 }
 size_t nufft_default_cg_max_iter(size_t n) { return nb::default_cg_max_iter(n); }
 
+// ------------------------------------------------------------ direct sums
+int nufft_nudft_direct_host(const double* x, size_t nx, const double* omega, const double* c, size_t n, double* f,
+                            int device) {
+    return guard([&] {
+        pick_device(device);
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf dx(8 * std::max<size_t>(nx, 1), s), dw(8 * std::max<size_t>(n, 1), s),
+            dc(16 * std::max<size_t>(n, 1), s), df(16 * std::max<size_t>(nx, 1), s);
+        NB_CUDA(cudaMemcpyAsync(dx.get(), x, 8 * nx, cudaMemcpyHostToDevice, s));
+        NB_CUDA(cudaMemcpyAsync(dw.get(), omega, 8 * n, cudaMemcpyHostToDevice, s));
+        NB_CUDA(cudaMemcpyAsync(dc.get(), c, 16 * n, cudaMemcpyHostToDevice, s));
+        nb::nudft_direct(dx.as<double>(), nx, dw.as<double>(), dc.as<double2>(), n, df.as<double2>(), s);
+        NB_CUDA(cudaMemcpyAsync(f, df.get(), 16 * nx, cudaMemcpyDeviceToHost, s));
+        NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+int nufft_nudft_direct(const double* x_dev, size_t nx, const double* omega_dev, const double* c_dev, size_t n,
+                       double* f_dev, void* stream) {
+    return guard([&] {
+        nb::nudft_direct(x_dev, nx, omega_dev, reinterpret_cast<const double2*>(c_dev), n,
+                         reinterpret_cast<double2*>(f_dev), as_stream(stream));
+    });
+}
+int nufft_nudft2d_direct_host(const double* x, const double* y, size_t count, const double* C, size_t m, size_t n,
+                              double* f, int device) {
+    return guard([&] {
+        if (m * n == 0) nb::throw_invalid("nudft2d_direct: inconsistent matrix dimensions");
+        pick_device(device);
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf dx(8 * std::max<size_t>(count, 1), s), dy(8 * std::max<size_t>(count, 1), s),
+            dC(16 * m * n, s), df(16 * std::max<size_t>(count, 1), s);
+        NB_CUDA(cudaMemcpyAsync(dx.get(), x, 8 * count, cudaMemcpyHostToDevice, s));
+        NB_CUDA(cudaMemcpyAsync(dy.get(), y, 8 * count, cudaMemcpyHostToDevice, s));
+        NB_CUDA(cudaMemcpyAsync(dC.get(), C, 16 * m * n, cudaMemcpyHostToDevice, s));
+        nb::nudft2d_direct(dx.as<double>(), dy.as<double>(), count, dC.as<double2>(), m, n, df.as<double2>(), s);
+        NB_CUDA(cudaMemcpyAsync(f, df.get(), 16 * count, cudaMemcpyDeviceToHost, s));
+        NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, size_t n_omega,
                        double epsilon, int device, nufft_plan3** out) {
     return guard([&] {

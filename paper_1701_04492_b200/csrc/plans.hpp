@@ -136,6 +136,12 @@ CgResult cg_solve_toeplitz(const ToeplitzState& op, const double2* rhs, double2*
                            size_t max_iter, std::vector<double>* history, cudaStream_t s);
 size_t default_cg_max_iter(size_t n);
 
+// ---- direct sums (direct.cu): oracle.hpp:70-107 on the device
+void nudft_direct(const double* x, size_t nx, const double* w, const double2* c, size_t n, double2* f,
+                  cudaStream_t s);
+void nudft2d_direct(const double* x, const double* y, size_t cnt, const double2* C, size_t m, size_t n,
+                    double2* f, cudaStream_t s);
+
 bool fused_2d_eligible(size_t m, size_t n, size_t count);
 void build_2d_fused(Plan2DState& st, cudaStream_t s);
 void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s);

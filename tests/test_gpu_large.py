@@ -169,3 +169,28 @@ def test_cfg5_direct_sum_spot_check(nb):
         ey = np.exp(-2j * np.pi * _exact_frac_phase(float(y[j]), ky))
         want = complex(ey @ (C2 @ ex))
         assert abs(f[j] - want) <= 1e-13 * rms, (j, abs(f[j] - want), rms)
+
+
+def test_cfg2_error_sweep_vs_gpu_direct(nb, cfg2):
+    """4096 outputs of the N = 2^24 transform against the GPU direct sum
+    (oracle.hpp:70-86 on the device): the eps = 1e-14 contract holds at scale."""
+    x, c = cfg2
+    p = nb.plan_nufft2(x, 1e-14)
+    f = nb.exec_nufft2(p, c)
+    idx = np.sort(np.random.default_rng(12).choice(N24, 4096, replace=False))
+    want = nb.nudft_direct(x[idx], np.arange(N24, dtype=np.float64), c)
+    rel = np.linalg.norm(f[idx] - want) / np.linalg.norm(want)
+    assert rel <= 1e-14, rel
+
+
+def test_cfg3_error_sweep_vs_gpu_direct(nb):
+    """Type I at 2^24: f_j = sum_k c_k exp(-2 pi i (j/N) w_k) for 2048 outputs."""
+    rng = np.random.default_rng(33)
+    d = rng.uniform(-0.5, 0.5, N24)
+    w = np.clip(np.arange(N24) + d, 0.0, float(N24))
+    c = rng.standard_normal(N24) + 1j * rng.standard_normal(N24)
+    f = nb.exec_nufft1(nb.plan_nufft1(w, 1e-14), c)
+    idx = np.sort(np.random.default_rng(13).choice(N24, 2048, replace=False))
+    want = nb.nudft_direct(idx / N24, w, c)
+    rel = np.linalg.norm(f[idx] - want) / np.linalg.norm(want)
+    assert rel <= 1e-14, rel

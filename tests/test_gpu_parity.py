@@ -243,3 +243,37 @@ def test_factor_mirrors_vs_oracle(nb, port):
     ko, uo, vo = port.build_factors(d, 0.25, np.arange(20) / 20, 1e-9)
     kg, ug, vg = nb.build_factors(d, 0.25, np.arange(20) / 20, 1e-9)
     assert ko == kg and np.max(np.abs(ug - uo)) <= 1e-14 and np.max(np.abs(vg - vo)) <= 1e-14
+
+
+# ------------------------------------------------------------------ GPU direct sums (oracle.hpp:70-107)
+def test_gpu_nudft_direct_vs_oracle(nb, port):
+    """The device direct sum (exact phase split, Neumaier, ascending k) against
+    the oracle's long-double-phase direct sum."""
+    for n in (1, 17, 1024, 3000):
+        rng = port.sampler(700 + n)
+        x = rng.uniform_vector(n, 0.0, 1.0)
+        w = rng.uniform_vector(n, 0.0, float(n))
+        c = rng.complex_vector(n)
+        assert rel_l2(nb.nudft_direct(x, w, c), port.nudft_direct(x, w, c)) <= 1e-15
+    m, nn, cnt = 24, 40, 300
+    rng = port.sampler(800)
+    x, y = rng.uniform_vector(cnt, 0.0, 1.0), rng.uniform_vector(cnt, 0.0, 1.0)
+    C2 = rng.complex_vector(m * nn).reshape(m, nn)
+    assert rel_l2(nb.nudft2d_direct(x, y, C2), port.nudft2d_direct(x, y, C2)) <= 1e-15
+
+
+def test_type2_large_vs_gpu_direct_sum(nb):
+    """Exact-error sweep at N = 2^18 the CPU oracle cannot reach in seconds:
+    every output of the fused type-II transform against the GPU direct sum,
+    within the reference's contract ||f - f_direct|| <= N eps ||c|| (with eps-level
+    actual agreement)."""
+    n = 1 << 18
+    rng = np.random.default_rng(18)
+    x = rng.random(n)
+    c = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for eps in (1e-14, 1e-9):
+        f = nb.exec_nufft2(nb.plan_nufft2(x, eps), c)
+        want = nb.nudft_direct(x, np.arange(n, dtype=np.float64), c)
+        err = np.linalg.norm(f - want)
+        assert err <= n * eps * np.linalg.norm(c)
+        assert err / np.linalg.norm(want) <= 10 * eps
