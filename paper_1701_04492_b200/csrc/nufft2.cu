@@ -852,25 +852,33 @@ __global__ void __launch_bounds__(TmShape<L2>::ALL, 1)
 //   EMPTY_b (named barrier, sample warps + next user of b): the gathers from b are done.
 // Each group loads its next Y row from HBM before waiting for its buffer and
 // has two sample periods per transform, so two transforms are in flight.
-template <int L2>
+template <int L2, int SWG = 1>
 struct G2Shape {
     static constexpr int G = L2 / 16;
-    static constexpr int S = 128;               // one sample warpgroup
-    static constexpr int Q = (18 * G / S + 3) / 4 * 4;  // samples per sample thread (capacity >= 1.125 L2)
+    static constexpr int S = 128 * SWG;         // sample warpgroups
+    static constexpr int CH = SWG == 1 ? 4 : 2;  // samples per TMEM chunk
+    static constexpr int Q = (18 * G / S + CH - 1) / CH * CH;  // samples per sample thread (capacity >= 1.125 L2)
     static constexpr int CAP = Q * S;
     static constexpr int ALL = 2 * G + S;
     // TMEM columns per sample: acc (4), h (2), t2 (1), Bessel state g_r, g_{r+1} (4)
-    static constexpr int COL_ACC = 0, COL_H = 4 * Q, COL_T = 6 * Q, COL_G = 7 * Q;
-    static constexpr unsigned TM_COLS = (11 * Q <= 128) ? 128u : (11 * Q <= 256 ? 256u : 512u);
+    static constexpr int COL_ACC = 0, COL_H = 4 * Q, COL_T = 6 * Q, COL_G = 7 * Q, COLS = 11 * Q;
+    static constexpr unsigned TM_COLS = (SWG * COLS <= 128) ? 128u : (SWG * COLS <= 256 ? 256u : 512u);
+    // registers: FFT groups 96, sample warps what is left of the CTA's allocation
+    // (SWG = 2 with setmaxnreg 96/48 was tried: ptxas compiled the whole kernel at
+    // the 768-thread launch bound of 80 registers and spilled 2.2 KB, so only
+    // SWG = 1 is instantiated)
+    static constexpr int REG_FFT = 96;
+    static constexpr int REG_SMP = SWG == 1 ? 96 : 48;
     static constexpr size_t SMEM = sizeof(double2) * (3 * padded_len(L2) + FftShapeX<L2>::TW_LEN);
-    static_assert(Q % 4 == 0 && 11 * Q <= 512, "sample layout");
+    static_assert(Q % CH == 0 && SWG * COLS <= 512, "sample layout");
     static_assert(SMEM <= 227 * 1024, "pass 2 (two groups) shared memory");
 };
 
-template <int L2, bool UNIFORM, bool DSRC>
-__global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
+template <int L2, bool UNIFORM, bool DSRC, int SWG>
+__global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
-    using W = G2Shape<L2>;
+    using W = G2Shape<L2, SWG>;
+    constexpr int CH = W::CH;
     constexpr int G = W::G;
     constexpr int S = W::S;
     constexpr int Q = W::Q;
@@ -890,7 +898,15 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    const unsigned tl = tm_lane_base(tmem_base);  // sample warps 2G/32.. map to quarters 0..3
+    if constexpr (W::REG_SMP != W::REG_FFT) {  // hand the sample warps' spare registers to the FFT groups
+        if (role < 2)
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(W::REG_FFT));
+        else
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(W::REG_SMP));
+    }
+    // sample warps 2G/32.. map to TMEM quarters (warp % 4); column block per extra warpgroup
+    const unsigned tl = tm_lane_base(tmem_base) +
+                        (unsigned)(role == 2 ? (tid >> 7) * W::COLS : 0);
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
     const long long n2 = 1ll << p.log_n2;
@@ -926,12 +942,12 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                 const double dn = (double)p.n;
                 // per-sample state into TMEM: acc = 0, h, t2
 #pragma unroll 1
-                for (int k = 0; k < Q / 4; ++k) {
-                    unsigned av[16], hv[8];
-                    unsigned t2v[4];
+                for (int k = 0; k < Q / CH; ++k) {
+                    unsigned av[4 * CH], hv[2 * CH];
+                    unsigned t2v[CH];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int i = tid + (4 * k + u) * S;
+                    for (int u = 0; u < CH; ++u) {
+                        const int i = tid + (CH * k + u) * S;
                         double h = 0.0;
                         int t2 = 0;
                         if (i < cnt) {
@@ -953,29 +969,29 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                         hv[2 * u + 1] = hi32(h);
                         t2v[u] = (unsigned)t2;
                     }
-                    tm_st16(tl + W::COL_ACC + 16 * k, av);
-                    tm_st8(tl + W::COL_H + 8 * k, hv);
-                    tm_st4(tl + W::COL_T + 4 * k, t2v[0], t2v[1], t2v[2], t2v[3]);
+                    tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                    tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+                    tm_stn<CH>(tl + W::COL_T + CH * k, t2v);
                     if constexpr (!UNIFORM) {
                         // (g_{r1-1}, g_{r1}) by the full series; lower orders follow from
                         // the backward recurrence g_{r-1} = r g_r - w g_{r+1}, stable for
                         // the minimal (Bessel) solution
-                        double w[4], ga[4], gb[4];
+                        double w[CH], ga[CH], gb[CH];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < CH; ++u) {
                             const double h = mk64(hv[2 * u], hv[2 * u + 1]);
                             w[u] = h * h;
                         }
-                        series_fixed<4, kSeriesTerms - 1>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms);
-                        series_fixed<4, kSeriesTerms - 1>(gb, w, kBes + p.r1 * kSeriesTerms);
+                        series_fixed<CH, kSeriesTerms - 1>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms);
+                        series_fixed<CH, kSeriesTerms - 1>(gb, w, kBes + p.r1 * kSeriesTerms);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < CH; ++u) {
                             av[4 * u] = lo32(ga[u]);
                             av[4 * u + 1] = hi32(ga[u]);
                             av[4 * u + 2] = lo32(gb[u]);
                             av[4 * u + 3] = hi32(gb[u]);
                         }
-                        tm_st16(tl + W::COL_G + 16 * k, av);
+                        tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, av);
                     }
                 }
                 tm_wait_st();
@@ -990,15 +1006,15 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                     (void)deg;
                     const double rd = (double)r;
 #pragma unroll 1
-                    for (int k = 0; k < ((p.ablate & 1) ? 0 : Q / 4); ++k) {
-                        unsigned av[16], gv[16], hv[8], t2v[4];
-                        tm_ld16(tl + W::COL_ACC + 16 * k, av);
-                        tm_ld8(tl + W::COL_H + 8 * k, hv);
-                        tm_ld4(tl + W::COL_T + 4 * k, t2v[0], t2v[1], t2v[2], t2v[3]);
-                        if constexpr (!UNIFORM) tm_ld16(tl + W::COL_G + 16 * k, gv);
+                    for (int k = 0; k < ((p.ablate & 1) ? 0 : Q / CH); ++k) {
+                        unsigned av[4 * CH], gv[4 * CH], hv[2 * CH], t2v[CH];
+                        tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                        tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+                        tm_ldn<CH>(tl + W::COL_T + CH * k, t2v);
+                        if constexpr (!UNIFORM) tm_ldn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
                         tm_wait_ld();
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < CH; ++u) {
                             const double2 X = xb[t2v[u]];
                             double2 acc;
                             if constexpr (UNIFORM) {
@@ -1022,8 +1038,8 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                             av[4 * u + 2] = lo32(acc.y);
                             av[4 * u + 3] = hi32(acc.y);
                         }
-                        tm_st16(tl + W::COL_ACC + 16 * k, av);
-                        if constexpr (!UNIFORM) tm_st16(tl + W::COL_G + 16 * k, gv);
+                        tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                        if constexpr (!UNIFORM) tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
                     }
                     // release b only to a later step (an EMPTY arrival nobody waits
                     // for would pair with the next use of the barrier)
@@ -1032,14 +1048,14 @@ __global__ void __launch_bounds__(G2Shape<L2>::ALL, 1)
                 tm_wait_st();
                 // f[perm] = 2 exp(2ih) (ih)^r0 acc
 #pragma unroll 1
-                for (int k = 0; k < Q / 4; ++k) {
-                    unsigned av[16], hv[8];
-                    tm_ld16(tl + W::COL_ACC + 16 * k, av);
-                    tm_ld8(tl + W::COL_H + 8 * k, hv);
+                for (int k = 0; k < Q / CH; ++k) {
+                    unsigned av[4 * CH], hv[2 * CH];
+                    tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                    tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
                     tm_wait_ld();
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int i = tid + (4 * k + u) * S;
+                    for (int u = 0; u < CH; ++u) {
+                        const int i = tid + (CH * k + u) * S;
                         if (i >= cnt) continue;
                         double2 out = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
                         if constexpr (!UNIFORM) {
@@ -1158,11 +1174,11 @@ void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1,
     NB_LAUNCH();
 }
 
-template <int L2, bool UNIFORM>
+template <int L2, bool UNIFORM, int SWG = 1>
 void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
-    constexpr size_t SM = G2Shape<L2>::SMEM;
-    constexpr int threads = G2Shape<L2>::ALL;
-    auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true> : k2_pass2_g2<L2, UNIFORM, false>;
+    constexpr size_t SM = G2Shape<L2, SWG>::SMEM;
+    constexpr int threads = G2Shape<L2, SWG>::ALL;
+    auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG> : k2_pass2_g2<L2, UNIFORM, false, SWG>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);

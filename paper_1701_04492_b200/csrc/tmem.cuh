@@ -73,6 +73,39 @@ __device__ __forceinline__ void tm_ld16(unsigned taddr, unsigned (&v)[16]) {
         : "r"(taddr)
         : "memory");
 }
+__device__ __forceinline__ void tm_st2(unsigned taddr, unsigned a, unsigned b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tm_ld2(unsigned taddr, unsigned& a, unsigned& b) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
+}
+// N consecutive columns, N in {2, 4, 8, 16}
+template <int N>
+__device__ __forceinline__ void tm_stn(unsigned taddr, const unsigned (&v)[N]) {
+    if constexpr (N == 2) {
+        tm_st2(taddr, v[0], v[1]);
+    } else if constexpr (N == 4) {
+        tm_st4(taddr, v[0], v[1], v[2], v[3]);
+    } else if constexpr (N == 8) {
+        tm_st8(taddr, v);
+    } else {
+        static_assert(N == 16, "tm_stn");
+        tm_st16(taddr, v);
+    }
+}
+template <int N>
+__device__ __forceinline__ void tm_ldn(unsigned taddr, unsigned (&v)[N]) {
+    if constexpr (N == 2) {
+        tm_ld2(taddr, v[0], v[1]);
+    } else if constexpr (N == 4) {
+        tm_ld4(taddr, v[0], v[1], v[2], v[3]);
+    } else if constexpr (N == 8) {
+        tm_ld8(taddr, v);
+    } else {
+        static_assert(N == 16, "tm_ldn");
+        tm_ld16(taddr, v);
+    }
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
