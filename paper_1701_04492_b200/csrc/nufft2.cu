@@ -254,12 +254,11 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             }
             gsync();  // previous term's last-stage reads of buf are done
             block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+            // y_index(rr, t1 = tid + q G, k2) = base(tid) + q G N2   (G even)
+            double2* yb = Y + y_index(r - p.r0, N, p.log_n2, tid, k2);
+            const long long ystride = (long long)G << p.log_n2;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const double2 w = cmul(base, step[q]);
-                const long long t1 = tid + q * G;
-                Y[y_index(r - p.r0, N, p.log_n2, t1, k2)] = cmul(v[q], w);
-            }
+            for (int q = 0; q < 16; ++q) yb[q * ystride] = cmul(v[q], cmul(base, step[q]));
         }
         tm_wait_st();
     }
