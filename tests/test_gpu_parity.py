@@ -277,3 +277,49 @@ def test_type2_large_vs_gpu_direct_sum(nb):
         err = np.linalg.norm(f - want)
         assert err <= n * eps * np.linalg.norm(c)
         assert err / np.linalg.norm(want) <= 10 * eps
+
+
+# ------------------------------------------------------------------ every fused shape
+@pytest.mark.parametrize("log_n", list(range(4, 23)))
+def test_pow2_sweep_type2_type1_adjoint_vs_gpu_direct(nb, log_n):
+    """Every power-of-two size selects a different kernel shape (N1 x N2 split,
+    single-pass N1 = 1, small/warp-specialized/two-group pass 2, one- or
+    two-worker pass 1 and transpose passes).  Each is checked against exact
+    direct sums on up to 512 outputs; eps = 1e-12 (K = 18) and ragged
+    (duplicate-bin, clustered-row) samples."""
+    n = 1 << log_n
+    rng = np.random.default_rng(1000 + log_n)
+    x = rng.random(n)
+    x[: n // 8] = (0.3 + rng.random(n // 8) * 4.0 / n) % 1.0   # crowded rows / duplicate bins
+    c = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    idx = np.sort(rng.choice(n, min(n, 512), replace=False))
+    k = np.arange(n, dtype=np.float64)
+    p = nb.plan_nufft2(x, 1e-12)
+    assert p.fused
+    f = nb.exec_nufft2(p, c)
+    want = nb.nudft_direct(x[idx], k, c)
+    assert rel_l2(f[idx], want) <= 1e-12
+    # adjoint: (A^H g)_k = sum_j g_j exp(+2 pi i x_j k)
+    g = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    a = nb.exec_nufft2_adjoint(p, g)
+    want_a = np.conj(nb.nudft_direct(idx.astype(np.float64), x, np.conj(g)))
+    assert rel_l2(a[idx], want_a) <= 1e-12
+    # type I on jittered frequencies: f_j = sum_k c_k exp(-2 pi i (j/N) w_k)
+    w = np.clip(k + rng.uniform(-0.5, 0.5, n), 0.0, float(n))
+    f1 = nb.exec_nufft1(nb.plan_nufft1(w, 1e-12), c)
+    want1 = nb.nudft_direct(idx / n, w, c)
+    assert rel_l2(f1[idx], want1) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(16, 4096), (4096, 16), (64, 1024), (1024, 64), (512, 512), (2048, 256)])
+def test_2d_fused_shapes_vs_gpu_direct(nb, m, n):
+    rng = np.random.default_rng(m * 7 + n)
+    cnt = m * n
+    x, y = rng.random(cnt), rng.random(cnt)
+    C2 = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    p = nb.plan_nufft2d2(x, y, m, n, 1e-12)
+    assert p.fused
+    f = nb.exec_nufft2d2(p, C2)
+    idx = np.sort(rng.choice(cnt, 256, replace=False))
+    want = nb.nudft2d_direct(x[idx], y[idx], C2)
+    assert rel_l2(f[idx], want) <= 1e-12
