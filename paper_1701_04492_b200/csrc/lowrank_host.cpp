@@ -163,4 +163,18 @@ std::vector<int> bessel_series_degrees(double gamma, std::size_t K) {
     return deg;
 }
 
+int bessel_series_degree_rel(double gamma, int r) {
+    const long double hmax = 3.14159265358979323846264338327950288L * gamma / 2.0L * (1.0L + 1e-12L);
+    const long double w = hmax * hmax;
+    const long double tol = std::ldexp(1.0L, -56);
+    const long double lower = 1.0L - w / (r + 1.0L);  // g_r r! >= 1 - w/(r+1) (alternating, decreasing)
+    if (!(lower > 0.0L)) return kSeriesTerms - 1;
+    for (int M = 0; M < kSeriesTerms; ++M) {
+        long double term = 1.0L;  // w^(M+1) r! / ((M+1)! (M+1+r)!)
+        for (int i = 1; i <= M + 1; ++i) term *= w / (static_cast<long double>(i) * static_cast<long double>(i + r));
+        if (term / lower <= tol) return M;
+    }
+    return kSeriesTerms - 1;
+}
+
 }  // namespace nb

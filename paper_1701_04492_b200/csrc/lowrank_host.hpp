@@ -36,5 +36,8 @@ const std::vector<double>& bessel_series_table();
 // smallest Horner degree M_r (<= 15) per r so that the truncated tail of
 // 2 |h|^r g_r stays below 2^-62 for |delta| <= gamma
 std::vector<int> bessel_series_degrees(double gamma, std::size_t K);
+// degree of g_r for full RELATIVE accuracy (truncation < 2^-56 of g_r) at |h| <= pi gamma / 2:
+// the starting values of the backward Bessel recurrence
+int bessel_series_degree_rel(double gamma, int r);
 
 }  // namespace nb

@@ -308,6 +308,7 @@ struct Pass2Params {
     unsigned long long* trace;  // diagnostics: per-iteration clock64 stamps of CTA 0 (nullptr = off)
     int ablate;                 // diagnostics (NUFFT_ABLATE): 1 skip sample math, 2 skip FFT math
     int deg[kRankCap];
+    int deg_rel0, deg_rel1;  // relative-accuracy degrees of g_{r1-1}, g_{r1} (recurrence start)
 };
 #define NB_TRACE(slot)                                                                   \
     do {                                                                                 \
@@ -981,8 +982,8 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                             const double h = mk64(hv[2 * u], hv[2 * u + 1]);
                             w[u] = h * h;
                         }
-                        series_fixed<CH, kSeriesTerms - 1>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms);
-                        series_fixed<CH, kSeriesTerms - 1>(gb, w, kBes + p.r1 * kSeriesTerms);
+                        series_deg<CH>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms, p.deg_rel0);
+                        series_deg<CH>(gb, w, kBes + p.r1 * kSeriesTerms, p.deg_rel1);
 #pragma unroll
                         for (int u = 0; u < CH; ++u) {
                             av[4 * u] = lo32(ga[u]);
@@ -1211,6 +1212,8 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.perm = pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
+    p.deg_rel0 = bessel_series_degree_rel(pl.gamma_factors, r1 - 1);
+    p.deg_rel1 = bessel_series_degree_rel(pl.gamma_factors, r1);
     static const bool trace = getenv("NUFFT_TRACE_PASS2") != nullptr;
     static const int ablate = getenv("NUFFT_ABLATE") ? atoi(getenv("NUFFT_ABLATE")) : 0;
     p.ablate = ablate;

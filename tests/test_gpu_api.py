@@ -179,3 +179,35 @@ def test_batch_and_term_ranges(nb, port):
     total = (parts[0] + parts[1] + parts[2]).cpu().numpy()
     assert rel_l2(total, full.cpu().numpy()) <= 1e-14
     assert rel_l2(full.cpu().numpy(), single[0]) == 0.0
+
+
+def test_batched_exec_equals_singles_all_types(nb):
+    """batch > 1 through the device entry points of type I, adjoint-free type III
+    and 2D: bit-identical to single executions (fused and generic shapes)."""
+    import torch
+    rng = np.random.default_rng(77)
+    dev = torch.device("cuda", 0)
+    for n in (1 << 12, 1000):
+        w = np.clip(np.arange(n) + rng.uniform(-0.4, 0.4, n), 0, n)
+        p1 = nb.plan_nufft1(w, 1e-12)
+        x = rng.random(n)
+        p3 = nb.plan_nufft3(x, rng.uniform(0, n, n), 1e-9)
+        for p in (p1, p3):
+            cs = torch.randn(3, n, dtype=torch.complex128, device=dev)
+            fb = torch.empty_like(cs)
+            p.execute_device(cs.data_ptr(), fb.data_ptr(), 3)
+            for b in range(3):
+                fs = torch.empty_like(cs[b])
+                p.execute_device(cs[b].data_ptr(), fs.data_ptr(), 1)
+                torch.cuda.synchronize()
+                assert torch.equal(torch.view_as_real(fs), torch.view_as_real(fb[b]))
+    m, nn, cnt = 64, 128, 5000
+    pd = nb.plan_nufft2d2(rng.random(cnt), rng.random(cnt), m, nn, 1e-12)
+    Cs = torch.randn(2, m, nn, dtype=torch.complex128, device=dev)
+    fb = torch.empty(2, cnt, dtype=torch.complex128, device=dev)
+    pd.execute_device(Cs.data_ptr(), fb.data_ptr(), 2)
+    for b in range(2):
+        fs = torch.empty(cnt, dtype=torch.complex128, device=dev)
+        pd.execute_device(Cs[b].data_ptr(), fs.data_ptr(), 1)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.view_as_real(fs), torch.view_as_real(fb[b]))
