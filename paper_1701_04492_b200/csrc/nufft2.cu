@@ -860,8 +860,8 @@ struct G2Shape {
     static constexpr int Q = (18 * G / S + CH - 1) / CH * CH;  // samples per sample thread (capacity >= 1.125 L2)
     static constexpr int CAP = Q * S;
     static constexpr int ALL = 2 * G + S;
-    // TMEM columns per sample: acc (4), h (2), t2 (1), Bessel state g_r, g_{r+1} (4)
-    static constexpr int COL_ACC = 0, COL_H = 4 * Q, COL_T = 6 * Q, COL_G = 7 * Q, COLS = 11 * Q;
+    // TMEM columns per sample: acc (4), h (2), t2 (1), Bessel state g_r, g_{r+1} (4), delta (2)
+    static constexpr int COL_ACC = 0, COL_H = 4 * Q, COL_T = 6 * Q, COL_G = 7 * Q, COL_D = 11 * Q, COLS = 13 * Q;
     static constexpr unsigned TM_COLS = (SWG * COLS <= 128) ? 128u : (SWG * COLS <= 256 ? 256u : 512u);
     // registers: FFT groups 96, sample warps what is left of the CTA's allocation
     // (SWG = 2 with setmaxnreg 96/48 was tried: ptxas compiled the whole kernel at
@@ -929,8 +929,13 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                     const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
                     double2 v[16];
+                    if (p.ablate & 4) {  // diagnostics: no Y loads
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                        for (int q = 0; q < 16; ++q) v[q] = make_double2(tid * 1e-3 + q, i * 1e-3);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    }
                     if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
                     if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                     gsync();  // last-stage reads of buf done
@@ -943,34 +948,37 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                 // per-sample state into TMEM: acc = 0, h, t2
 #pragma unroll 1
                 for (int k = 0; k < Q / CH; ++k) {
-                    unsigned av[4 * CH], hv[2 * CH];
+                    unsigned av[4 * CH], hv[2 * CH], dv[2 * CH];
                     unsigned t2v[CH];
 #pragma unroll
                     for (int u = 0; u < CH; ++u) {
                         const int i = tid + (CH * k + u) * S;
-                        double h = 0.0;
+                        double d = 0.0;
                         int t2 = 0;
                         if (i < cnt) {
                             if constexpr (DSRC) {  // type-I core: stored delta and key
-                                h = half_phase(p.ds[cb + i]);
+                                d = p.ds[cb + i];
                                 t2 = (int)(p.skey[cb + i] & ((1u << p.log_n2) - 1u));
                             } else {
                                 const double x = p.xs[cb + i];
                                 const double pr = __dmul_rn(dn, x);
                                 const long long sj = (long long)round(pr);
-                                const double d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                                d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
                                 t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
-                                h = half_phase(d);
                             }
                         }
+                        const double h = half_phase(d);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
                         hv[2 * u] = lo32(h);
                         hv[2 * u + 1] = hi32(h);
+                        dv[2 * u] = lo32(d);
+                        dv[2 * u + 1] = hi32(d);
                         t2v[u] = (unsigned)t2;
                     }
                     tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
                     tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+                    tm_stn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
                     tm_stn<CH>(tl + W::COL_T + CH * k, t2v);
                     if constexpr (!UNIFORM) {
                         // (g_{r1-1}, g_{r1}) by the full series; lower orders follow from
@@ -1049,9 +1057,10 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                 // f[perm] = 2 exp(2ih) (ih)^r0 acc
 #pragma unroll 1
                 for (int k = 0; k < Q / CH; ++k) {
-                    unsigned av[4 * CH], hv[2 * CH];
+                    unsigned av[4 * CH], hv[2 * CH], dv[2 * CH];
                     tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
                     tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+                    tm_ldn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
                     tm_wait_ld();
 #pragma unroll
                     for (int u = 0; u < CH; ++u) {
@@ -1071,8 +1080,8 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                                     default: break;
                                 }
                             }
-                            double sn, cs;
-                            sincos(2.0 * h, &sn, &cs);
+                            double sn, cs;  // exp(2ih) = exp(-i pi delta), argument exact
+                            sincospi(-mk64(dv[2 * u], dv[2 * u + 1]), &sn, &cs);
                             out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
                         }
                         __stcs(f + p.perm[cb + i], out);
