@@ -287,16 +287,19 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     dom = ("k2_pass2", p2_bytes, ms2) if ms2 >= ms1 else ("k2_pass1", p1_bytes, ms1)
     achieved = dom[1] / (dom[2] / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_kernel = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(dom[0])
+        try:  # ncu dram read+write of the same kernel (its template instance name starts with dom[0])
+            for name, val in json.load(open(tpath)).items():
+                if name.startswith(dom[0]):
+                    traffic, traffic_kernel = val, name
+                    break
         except Exception:
             traffic = None
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": traffic, "kernel": dom[0],
+        "frac": achieved / peak, "traffic": traffic, "kernel": traffic_kernel or dom[0],
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": dom[1],
         "per_pass_ms": {"k2_pass1": ms1, "k2_pass2": ms2},
