@@ -321,6 +321,69 @@ __device__ __forceinline__ void block_fft_1buf(double2 (&v)[16], double2* buf, i
     }
 }
 
+// ------------------------------------------------------------ two-level 4096
+// 4096 = 16 x 256 with one group-wide exchange.  j = j0 + 256 j1, k = k1 + 16 k0:
+//   A[j0, k1] = w_4096^{j0 k1} sum_j1 x[j0 + 256 j1] w_16^{j1 k1}   (thread j0, registers)
+//   X[k1 + 16 k0] = sum_j0 A[j0, k1] w_256^{j0 k0}                  (16 independent 256-pt DFTs)
+// The transpose A -> (k1-major) is the only exchange every thread of the group
+// takes part in (write, barrier, read).  Each 256-point DFT then belongs to a
+// sub-group of 16 threads of one warp (g = k1): radix 16 over j0 = u + 16 m,
+// twiddle w_256^{u a}, and a 16 x 16 transpose inside the sub-group's own
+// 272-element region of the same buffer that needs only __syncwarp.  Two
+// group barriers per transform instead of four for block_fft_1buf; same FP64
+// work.
+//
+// Sub-groups interleave in the warp (lane = 2u + (g & 1)), so lanes 2i, 2i+1
+// hold outputs t and t + 1 — both halves of a 32-byte sector sit in one
+// quarter-warp of a 16-byte store.  Odd regions XOR their slot index with 4
+// (bijective inside each aligned 8-slot block) so the two sub-groups of a
+// quarter-warp touch complementary bank halves: every exchange access is
+// conflict-free.
+//
+// In:  v[q] = x[tid + 256 q].   Out: v[b] = X[g + 16 u + 256 b] (fft2l_out_index).
+// The thread's last reads are the 16 slots fft2l_slot(tid, b) of buf, so it
+// may overwrite exactly those (e.g. with X) without a barrier; anything else
+// needs a group barrier first.  buf: padded_len(4096) = 16 regions x 272.
+constexpr int kR2l = 272;  // region stride (17 x 16)
+
+__device__ __forceinline__ int fft2l_g(int tid) { return ((tid >> 5) << 1) | (tid & 1); }
+__device__ __forceinline__ int fft2l_u(int tid) { return (tid >> 1) & 15; }
+__host__ __device__ __forceinline__ int fft2l_swz(int g) { return (g & 1) << 2; }
+__device__ __forceinline__ int fft2l_out_index(int tid, int b) { return fft2l_g(tid) + 16 * fft2l_u(tid) + 256 * b; }
+// buffer slot of X[t] after block_fft_2l when the owner writes it in place
+__host__ __device__ __forceinline__ int fft2l_slot_of(int t) {
+    const int g = t & 15, a = (t >> 4) & 15, b = t >> 8;
+    return g * kR2l + ((17 * a + b) ^ fft2l_swz(g));
+}
+__device__ __forceinline__ int fft2l_slot(int tid, int b) {
+    const int g = fft2l_g(tid);
+    return g * kR2l + ((17 * fft2l_u(tid) + b) ^ fft2l_swz(g));
+}
+
+template <int SIGN, class Bar>
+__device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
+                                             Bar bar) {
+    dft<16, SIGN>(v);
+    apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) buf[k1 * kR2l + (tid ^ fft2l_swz(k1))] = v[k1];
+    bar();
+    const int g = fft2l_g(tid), u = fft2l_u(tid), sw = fft2l_swz(g);
+    double2* reg = buf + g * kR2l;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = reg[(u + 16 * m) ^ sw];
+    dft<16, SIGN>(v);
+#pragma unroll
+    for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], tw_sign<SIGN>(T.t16[a * 16 + u]));
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < 16; ++a) reg[(17 * a + u) ^ sw] = v[a];
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < 16; ++w) v[w] = reg[(17 * u + w) ^ sw];
+    dft<16, SIGN>(v);
+}
+
 // the buffer that is NOT read by the final stage (safe to overwrite after
 // block_fft returns, once every thread of the group has passed the last barrier)
 template <int L>

@@ -162,9 +162,14 @@ struct P1TmShape {
     static_assert((THREADS / 32 + 3) / 4 * 128 <= 512, "TMEM columns");
 };
 
-template <int L1, bool UNIFORM>
+// F2L (L1 = 4096): the column FFT is block_fft_2l (two group barriers per
+// term instead of four); each thread then holds outputs t1 = t1_0 + 256 q with
+// t1_0 = fft2l_out_index(tid, 0), lanes 2i and 2i + 1 the two rows of one
+// 32-byte Y sector.
+template <int L1, bool UNIFORM, bool F2L = false>
 __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     k2_pass1_tm(const double2* __restrict__ c, double2* __restrict__ Y, Pass1Params p) {
+    static_assert(!F2L || L1 == 4096, "two-level FFT is 4096-point");
     constexpr int G = L1 / 16;
     extern __shared__ double2 smem[];
     __shared__ unsigned tmem_base;
@@ -189,7 +194,8 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
         gsync();  // previous column's readers of step are done
         for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
-        const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
+        const int t1_0 = F2L ? fft2l_out_index(tid, 0) : tid;                 // first output row
+        const double2 base = unit_root(k2 * t1_0, N);                         // w_N^{k2 t1_0}
         const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
         // column of c and the Chebyshev state (T_{r0-1}, T_r0) into TMEM
 #pragma unroll
@@ -253,9 +259,13 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 }
             }
             gsync();  // previous term's last-stage reads of buf are done
-            block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
-            // y_index(rr, t1 = tid + q G, k2) = base(tid) + q G N2   (G even)
-            double2* yb = Y + y_index(r - p.r0, N, p.log_n2, tid, k2);
+            if constexpr (F2L) {
+                block_fft_2l<-1>(v, buf, tid, T, gsync);
+            } else {
+                block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+            }
+            // y_index(rr, t1 = t1_0 + q G, k2) = base(t1_0) + q G N2   (G even)
+            double2* yb = Y + y_index(r - p.r0, N, p.log_n2, t1_0, k2);
             const long long ystride = (long long)G << p.log_n2;
 #pragma unroll
             for (int q = 0; q < 16; ++q) yb[q * ystride] = cmul(v[q], cmul(base, step[q]));
@@ -874,9 +884,14 @@ struct G2Shape {
     static_assert(SMEM <= 227 * 1024, "pass 2 (two groups) shared memory");
 };
 
-template <int L2, bool UNIFORM, bool DSRC, int SWG>
+// F2L (L2 = 4096): the row FFT is block_fft_2l (two group barriers per step
+// instead of four plus one before the X write): each thread writes its X
+// values into the buffer slots it read last (fft2l_slot), and samples store
+// their gather slot fft2l_slot_of(t2) in TMEM instead of t2.
+template <int L2, bool UNIFORM, bool DSRC, int SWG, bool F2L = false>
 __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
+    static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
     using W = G2Shape<L2, SWG>;
     constexpr int CH = W::CH;
     constexpr int G = W::G;
@@ -937,10 +952,17 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                         for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
                     }
                     if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
-                    if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
-                    gsync();  // last-stage reads of buf done
+                    if constexpr (F2L) {
+                        if (!(p.ablate & 2)) block_fft_2l<-1>(v, buf, tid, T, gsync);
+                        // X in place: each thread overwrites only the slots it read last
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                        for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
+                    } else {
+                        if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                        gsync();  // last-stage reads of buf done
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    }
                     nbar_arrive(BAR_FULL + b, PAIR);
                 }
             } else {
@@ -974,7 +996,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                         hv[2 * u + 1] = hi32(h);
                         dv[2 * u] = lo32(d);
                         dv[2 * u + 1] = hi32(d);
-                        t2v[u] = (unsigned)t2;
+                        t2v[u] = (unsigned)(F2L ? fft2l_slot_of(t2) : t2);
                     }
                     tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
                     tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
@@ -1122,7 +1144,7 @@ int occupancy(const void* fn, int threads, size_t smem) {
 inline int pass1_variant() {
     static const int v = [] {
         const char* e = getenv("NUFFT_PASS1_VARIANT");
-        return e ? atoi(e) : 1;
+        return e ? atoi(e) : 2;
     }();
     return v;
 }
@@ -1132,10 +1154,13 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
                   cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     if constexpr (L1 >= 2048) {
-        if (pass1_variant() == 1) {
+        if (pass1_variant() >= 1) {
             constexpr size_t SMT = P1TmShape<L1>::SMEM;
             Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
             auto fn = pl.uniform ? k2_pass1_tm<L1, true> : k2_pass1_tm<L1, false>;
+            if constexpr (L1 == 4096) {
+                if (pass1_variant() == 2) fn = pl.uniform ? k2_pass1_tm<L1, true, true> : k2_pass1_tm<L1, false, true>;
+            }
             set_smem(fn, SMT);
             const long long n2 = 1ll << pl.bk.log_n2;
             const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
@@ -1171,6 +1196,16 @@ inline int pass2_variant() {
     return v;
 }
 
+// NUFFT_PASS2_FFT2L=0 selects the three-stage block FFT in the default pass-2
+// kernel (A/B switch for the two-level FFT)
+inline bool pass2_fft2l() {
+    static const bool v = [] {
+        const char* e = getenv("NUFFT_PASS2_FFT2L");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 template <int L2, bool UNIFORM, int X2, bool STAGE>
 void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms,
                cudaStream_t s) {
@@ -1188,6 +1223,10 @@ void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1,
     constexpr size_t SM = G2Shape<L2, SWG>::SMEM;
     constexpr int threads = G2Shape<L2, SWG>::ALL;
     auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG> : k2_pass2_g2<L2, UNIFORM, false, SWG>;
+    if constexpr (L2 == 4096) {
+        if (pass2_fft2l())
+            fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG, true> : k2_pass2_g2<L2, UNIFORM, false, SWG, true>;
+    }
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);
