@@ -329,35 +329,38 @@ __device__ __forceinline__ void block_fft_1buf(double2 (&v)[16], double2* buf, i
 // takes part in (write, barrier, read).  Each 256-point DFT then belongs to a
 // sub-group of 16 threads of one warp (g = k1): radix 16 over j0 = u + 16 m,
 // twiddle w_256^{u a}, and a 16 x 16 transpose inside the sub-group's own
-// 272-element region of the same buffer that needs only __syncwarp.  Two
+// 256-element region of the same buffer that needs only __syncwarp.  Two
 // group barriers per transform instead of four for block_fft_1buf; same FP64
-// work.
+// work; no padding (4096 slots).
 //
 // Sub-groups interleave in the warp (lane = 2u + (g & 1)), so lanes 2i, 2i+1
 // hold outputs t and t + 1 — both halves of a 32-byte sector sit in one
-// quarter-warp of a 16-byte store.  Odd regions XOR their slot index with 4
-// (bijective inside each aligned 8-slot block) so the two sub-groups of a
-// quarter-warp touch complementary bank halves: every exchange access is
-// conflict-free.
+// quarter-warp of a 16-byte store.  Slots are XOR-swizzled inside aligned
+// 8-slot blocks (16-byte slots, 8 per 128-byte bank row): region g uses
+// swz(g) = 4 (g & 1) | ((g >> 1) & 3), so the two sub-groups of a quarter-warp
+// always touch complementary bank halves (every exchange access conflict-free),
+// and the exchange-2 slots are further XORed with (a & 7) so a column read
+// of the 16 x 16 tile is conflict-free.  X[t] of the thread's outputs ends in
+// the slots it read last (fft2l_slot); since swz(g) is a bijection on every 8
+// consecutive g, gathers of consecutive t (sorted samples) spread over all banks.
 //
 // In:  v[q] = x[tid + 256 q].   Out: v[b] = X[g + 16 u + 256 b] (fft2l_out_index).
-// The thread's last reads are the 16 slots fft2l_slot(tid, b) of buf, so it
-// may overwrite exactly those (e.g. with X) without a barrier; anything else
-// needs a group barrier first.  buf: padded_len(4096) = 16 regions x 272.
-constexpr int kR2l = 272;  // region stride (17 x 16)
+// The thread may overwrite exactly its 16 slots fft2l_slot(tid, b) (e.g. with
+// X) without a barrier; anything else needs a group barrier first.
+constexpr int kBuf2l = 4096;  // buffer slots (double2)
 
 __device__ __forceinline__ int fft2l_g(int tid) { return ((tid >> 5) << 1) | (tid & 1); }
 __device__ __forceinline__ int fft2l_u(int tid) { return (tid >> 1) & 15; }
-__host__ __device__ __forceinline__ int fft2l_swz(int g) { return (g & 1) << 2; }
+__host__ __device__ __forceinline__ int fft2l_swz(int g) { return ((g & 1) << 2) | ((g >> 1) & 3); }
 __device__ __forceinline__ int fft2l_out_index(int tid, int b) { return fft2l_g(tid) + 16 * fft2l_u(tid) + 256 * b; }
-// buffer slot of X[t] after block_fft_2l when the owner writes it in place
+// slot of X[t] after block_fft_2l when every owner writes its outputs in place
 __host__ __device__ __forceinline__ int fft2l_slot_of(int t) {
     const int g = t & 15, a = (t >> 4) & 15, b = t >> 8;
-    return g * kR2l + ((17 * a + b) ^ fft2l_swz(g));
+    return g * 256 + 16 * a + (b ^ fft2l_swz(g) ^ (a & 7));
 }
 __device__ __forceinline__ int fft2l_slot(int tid, int b) {
-    const int g = fft2l_g(tid);
-    return g * kR2l + ((17 * fft2l_u(tid) + b) ^ fft2l_swz(g));
+    const int g = fft2l_g(tid), u = fft2l_u(tid);
+    return g * 256 + 16 * u + (b ^ fft2l_swz(g) ^ (u & 7));
 }
 
 template <int SIGN, class Bar>
@@ -366,21 +369,25 @@ __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int
     dft<16, SIGN>(v);
     apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
 #pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) buf[k1 * kR2l + (tid ^ fft2l_swz(k1))] = v[k1];
+    for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 256 + (tid ^ fft2l_swz(k1))] = v[k1];
     bar();
     const int g = fft2l_g(tid), u = fft2l_u(tid), sw = fft2l_swz(g);
-    double2* reg = buf + g * kR2l;
+    double2* reg = buf + g * 256;
+    const double2* rd1 = reg + (u ^ sw);
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = reg[(u + 16 * m) ^ sw];
+    for (int m = 0; m < 16; ++m) v[m] = rd1[16 * m];
     dft<16, SIGN>(v);
 #pragma unroll
     for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], tw_sign<SIGN>(T.t16[a * 16 + u]));
     __syncwarp();
+    const int U = u ^ sw;
 #pragma unroll
-    for (int a = 0; a < 16; ++a) reg[(17 * a + u) ^ sw] = v[a];
+    for (int a = 0; a < 16; ++a) reg[16 * a + (U ^ (a & 7))] = v[a];
     __syncwarp();
+    double2* rd2 = reg + 16 * u;
+    const int A = sw ^ (u & 7);
 #pragma unroll
-    for (int w = 0; w < 16; ++w) v[w] = reg[(17 * u + w) ^ sw];
+    for (int w = 0; w < 16; ++w) v[w] = rd2[w ^ A];
     dft<16, SIGN>(v);
 }
 
