@@ -888,7 +888,14 @@ struct G2Shape {
 // instead of four plus one before the X write): each thread writes its X
 // values into the buffer slots it read last (fft2l_slot), and samples store
 // their gather slot fft2l_slot_of(t2) in TMEM instead of t2.
-template <int L2, bool UNIFORM, bool DSRC, int SWG, bool F2L = false>
+//
+// CONT: one continuous step sequence over all (row, chunk) units of the CTA
+// (global step S: buffer S % 3, FFT group S % 2) instead of a CTA barrier
+// after every unit, so the FFT groups run up to three steps into the next row
+// while the sample warps finish the last Horner steps, write f and set up the
+// next row's samples.  The groups end with the EMPTY waits of three virtual
+// steps so every sample arrival is matched.
+template <int L2, bool UNIFORM, bool DSRC, int SWG, bool F2L = false, bool CONT = false>
 __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
     static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
@@ -925,6 +932,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
     const long long n2 = 1ll << p.log_n2;
+    int S0 = 0;  // CONT: global index of the unit's first step
     for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         for (int cb = beg; cb < end; cb += CAP) {
@@ -933,8 +941,9 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
             if (role < 2) {
                 const int bar = BAR_GRP + role;
                 auto gsync = [bar] { nbar_sync(bar, G); };
-                for (int i = role; i < nt; i += 2) {
-                    const int b = i % 3;
+                const int boff = CONT ? S0 % 3 : 0;
+                for (int i = CONT ? ((role - S0) & 1) : role; i < nt; i += 2) {
+                    const int b = (i + boff) % 3;
                     double2* buf = bufs + b * padded_len(L2);
                     const int rr = p.r1 - 1 - i - p.r0;
                     if (tid == 0 && i + 2 < nt) {  // warm L2 with this group's next row
@@ -951,7 +960,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
 #pragma unroll
                         for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
                     }
-                    if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step i-3 from b done
+                    if ((CONT ? S0 + i : i) >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step -3 from b done
                     if constexpr (F2L) {
                         if (!(p.ablate & 2)) block_fft_2l<-1>(v, buf, tid, T, gsync);
                         // X in place: each thread overwrites only the slots it read last
@@ -1025,9 +1034,10 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                 }
                 tm_wait_st();
+                const int boff = CONT ? S0 % 3 : 0;
                 for (int i = 0; i < nt; ++i) {
                     const int r = p.r1 - 1 - i;
-                    const int b = i % 3;
+                    const int b = (i + boff) % 3;
                     const double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, PAIR);
                     const double* a = kBes + r * kSeriesTerms;
@@ -1073,7 +1083,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                     // release b only to a later step (an EMPTY arrival nobody waits
                     // for would pair with the next use of the barrier)
-                    if (i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
+                    if (CONT || i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
                 }
                 tm_wait_st();
                 // f[perm] = 2 exp(2ih) (ih)^r0 acc
@@ -1110,12 +1120,305 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                 }
             }
-            __syncthreads();  // buffers and TMEM state free for the next chunk
+            if constexpr (CONT) {
+                S0 += nt;
+            } else {
+                __syncthreads();  // buffers and TMEM state free for the next chunk
+            }
         }
+    }
+    if constexpr (CONT) {  // match the sample warps' EMPTY arrivals of the last three steps
+        if (role < 2)
+            for (int sv = S0; sv < S0 + 3; ++sv)
+                if ((sv & 1) == role && sv >= 3) nbar_sync(BAR_EMPTY + sv % 3, PAIR);
     }
     tm_fence_before();
     __syncthreads();
     if (role == 2 && tid < 32) tm_dealloc(tmem_base, W::TM_COLS);
+}
+
+// ---------------------------------------------------------------- fused samples
+// Pass 2 (L2 = 4096) without a sample warpgroup: two FFT groups of 256
+// threads (128 registers each) take the steps S of one continuous sequence
+// over the CTA's (row, chunk) units in turn (group S % 2), and each group
+// updates every sample of the unit right after its own row FFT:
+//   FFT_r (block_fft_2l, X left in place in the group's own buffer)
+//   -> wait for the other group's update of step S-1   (named barrier H)
+//   -> acc <- acc (i h) + g_r X_r[t2], g_{r-1} = r g_r - w g_{r+1}  (TMEM state)
+//   -> hand off to the other group                      (named barrier H)
+// The FFT of one group overlaps the sample update of the other (FP64-dense
+// butterflies next to latency-bound gathers), the update is spread over 256
+// threads instead of 128, the row spectra never leave their group's buffer,
+// and no group waits for a whole-CTA barrier inside a row.  At a unit
+// boundary the group that did the last update writes f for half the samples
+// and sets up half of the next unit's, while the other group transforms the
+// first row of the next unit and then does the other halves.
+// Sample slot j of thread t is unit sample t + 256 j; its state lives in the
+// thread's TMEM lane (shared by the same t of both groups), 13 columns:
+// acc (4), g_r, g_{r+1} (4), h (2), gather slot (1), delta (2).
+struct FsShape {
+    static constexpr int G = 256;
+    static constexpr int SLOTS = 18;  // CAP = 4608 = 1.125 x 4096 samples per unit
+    static constexpr int CAP = SLOTS * G;
+    static constexpr int CH = 2;      // samples per TMEM chunk
+    static constexpr int COL_ACC = 0, COL_G = 4 * SLOTS, COL_H = 8 * SLOTS, COL_T = 10 * SLOTS,
+                         COL_D = 11 * SLOTS, COLS = 13 * SLOTS;
+    static constexpr size_t SMEM = sizeof(double2) * (2 * kBuf2l + FftShapeX<4096>::TW_LEN);
+    static_assert(COLS <= 256 && SLOTS % CH == 0, "TMEM layout");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+// load one Y row (stride-2 layout, y_index), transform it and leave X_r in
+// place in the group's buffer (fft2l_slot order)
+template <class Bar>
+__device__ __forceinline__ void fs_fft_row(const double2* row_in, double2* buf, int tid, const Twiddles<4096>& T,
+                                           Bar gsync) {
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * 256));
+    gsync();  // the group's gathers from its buffer (its previous step) are done
+    block_fft_2l<-1>(v, buf, tid, T, gsync);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
+    gsync();  // X complete
+}
+
+template <bool UNIFORM, bool DSRC>
+__global__ void __launch_bounds__(512, 1)
+    k2_pass2_fs(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
+    using W = FsShape;
+    constexpr int L2 = 4096, G = 256, CH = W::CH;
+    constexpr int BAR_G = 1, BAR_H = 3, BAR_E = 5, BAR_U = 6;  // groups 1-2, handoff 3-4 (by arriving group)
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x >> 8;
+    const int tid = threadIdx.x & (G - 1);
+    double2* buf = smem + grp * kBuf2l;
+    double2* tw = smem + 2 * kBuf2l;
+    twiddle_table_build<L2>(tw, threadIdx.x, 2 * G);
+    Twiddles<L2> T;
+    twiddle_init<L2>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tl = tm_lane_base(tmem_base) + (unsigned)(((tid >> 7) & 1) * 256);
+    const int gbar = BAR_G + grp;
+    auto gsync = [gbar] { nbar_sync(gbar, G); };
+    const long long N = p.n;
+    const long long n1 = 1ll << p.log_n1;
+    const int nt = p.r1 - p.r0;
+    const double dn = (double)p.n;
+
+    // per-sample state of chunk k (slots CH k .. CH k + CH - 1) of a unit
+    auto init_chunk = [&](int cb, int cnt, int k) {
+        unsigned av[4 * CH], hv[2 * CH], dv[2 * CH], t2v[CH];
+        double h[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+            const int i = tid + (CH * k + u) * G;
+            double d = 0.0;
+            int t2 = 0;
+            if (i < cnt) {
+                if constexpr (DSRC) {  // type-I core: stored delta and key
+                    d = p.ds[cb + i];
+                    t2 = (int)(p.skey[cb + i] & ((1u << p.log_n2) - 1u));
+                } else {
+                    const double x = p.xs[cb + i];
+                    const double pr = __dmul_rn(dn, x);
+                    const long long sj = (long long)round(pr);
+                    d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                    t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
+                }
+            }
+            h[u] = half_phase(d);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
+            hv[2 * u] = lo32(h[u]);
+            hv[2 * u + 1] = hi32(h[u]);
+            dv[2 * u] = lo32(d);
+            dv[2 * u + 1] = hi32(d);
+            t2v[u] = (unsigned)fft2l_slot_of(t2);
+        }
+        tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+        tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+        tm_stn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
+        tm_stn<CH>(tl + W::COL_T + CH * k, t2v);
+        if constexpr (!UNIFORM) {
+            // (g_{r1-1}, g_{r1}) by the series; lower orders by the backward recurrence
+            double w[CH], ga[CH], gb[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) w[u] = h[u] * h[u];
+            series_deg<CH>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms, p.deg_rel0);
+            series_deg<CH>(gb, w, kBes + p.r1 * kSeriesTerms, p.deg_rel1);
+            unsigned gv[4 * CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                gv[4 * u] = lo32(ga[u]);
+                gv[4 * u + 1] = hi32(ga[u]);
+                gv[4 * u + 2] = lo32(gb[u]);
+                gv[4 * u + 3] = hi32(gb[u]);
+            }
+            tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+        }
+    };
+    // f[perm] = 2 exp(2ih) (ih)^r0 acc for chunk k
+    auto epi_chunk = [&](int cb, int cnt, int k) {
+        unsigned av[4 * CH], hv[2 * CH], dv[2 * CH];
+        tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+        tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+        tm_ldn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
+        tm_wait_ld();
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+            const int i = tid + (CH * k + u) * G;
+            if (i >= cnt) continue;
+            double2 out = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+            if constexpr (!UNIFORM) {
+                const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                if (p.r0 > 0) {
+                    double hr = 1.0;
+                    for (int m = 0; m < p.r0; ++m) hr *= h;
+                    out = cscale(out, hr);
+                    switch (p.r0 & 3) {
+                        case 1: out = make_double2(-out.y, out.x); break;
+                        case 2: out = make_double2(-out.x, -out.y); break;
+                        case 3: out = make_double2(out.y, -out.x); break;
+                        default: break;
+                    }
+                }
+                double sn, cs;  // exp(2ih) = exp(-i pi delta), argument exact
+                sincospi(-mk64(dv[2 * u], dv[2 * u + 1]), &sn, &cs);
+                out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+            }
+            __stcs(f + p.perm[cb + i], out);
+        }
+    };
+    // set-up and write-out are split between the groups by chunk parity (the
+    // same chunks in every unit, so no group re-initializes a chunk the other
+    // one is still writing out)
+    auto nchunks = [](int c) { return ((c + G - 1) / G + CH - 1) / CH; };
+    // first unit of the CTA
+    long long row = blockIdx.x;
+    int cb = 0, cnt = 0;
+    auto seek = [&](long long r, int c) {  // first non-empty unit at or after (row r, sample c)
+        for (; r < n1; r += gridDim.x) {
+            const int beg = p.rowoff[r], end = p.rowoff[r + 1];
+            const int c0 = c < 0 ? beg : c;
+            if (c0 < end) {
+                row = r;
+                cb = c0;
+                cnt = min(W::CAP, end - c0);
+                return;
+            }
+            c = -1;
+        }
+        row = n1;
+    };
+    seek(row, -1);
+    if (row < n1) {
+        for (int k = grp; k < nchunks(cnt); k += 2) init_chunk(cb, cnt, k);
+        tm_wait_st();
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    auto fft_row = [&](const double2* row_in) { fs_fft_row(row_in, buf, tid, T, gsync); };
+    int S0 = 0;        // global index of the unit's first step
+    bool pre = false;  // this group's first step of the unit is already transformed
+    while (row < n1) {
+        const long long urow = row;
+        const int ucb = cb, ucnt = cnt;
+        const int nch = nchunks(ucnt);  // occupied chunks (CTA-uniform)
+        // the next unit: the rest of this row, else the CTA's next non-empty row
+        if (ucb + ucnt < p.rowoff[urow + 1])
+            seek(urow, ucb + ucnt);
+        else
+            seek(urow + gridDim.x, -1);
+        const bool has_next = row < n1;
+        const int last = nt - 1;
+        const int lastgrp = (S0 + last) & 1;  // group of the unit's last update
+        for (int i = (grp - S0) & 1; i < nt; i += 2) {
+            const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
+            const int r = p.r1 - 1 - i;
+            if (i > 0 || !pre) {
+                if (tid == 0 && i + 2 < nt) {  // warm L2 with this group's next row
+                    const void* nxt = Y + y_index(rr - 2, N, p.log_n2, urow, 0);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                                 "r"((unsigned)(2 * L2 * sizeof(double2))) : "memory");
+                }
+                fft_row(Y + y_index(rr, N, p.log_n2, urow, 0));
+            }
+            if (i > 0) {  // the other group's update of step i-1 is done
+                nbar_sync(BAR_H + (grp ^ 1), 2 * G);
+                tm_fence_after();
+            }
+            const double rd = (double)r;
+#pragma unroll 1
+            for (int k = 0; k < nch; ++k) {
+                unsigned av[4 * CH], gv[4 * CH], hv[2 * CH], t2v[CH];
+                tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+                tm_ldn<CH>(tl + W::COL_T + CH * k, t2v);
+                if constexpr (!UNIFORM) tm_ldn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+                tm_wait_ld();
+#pragma unroll
+                for (int u = 0; u < CH; ++u) {
+                    const double2 X = buf[t2v[u]];
+                    double2 acc;
+                    if constexpr (UNIFORM) {
+                        acc = X;
+                    } else {
+                        const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                        const double gr = mk64(gv[4 * u], gv[4 * u + 1]);
+                        const double gr1 = mk64(gv[4 * u + 2], gv[4 * u + 3]);
+                        const double ax = mk64(av[4 * u], av[4 * u + 1]);
+                        const double ay = mk64(av[4 * u + 2], av[4 * u + 3]);
+                        acc.x = __fma_rn(gr, X.x, -h * ay);
+                        acc.y = __fma_rn(gr, X.y, h * ax);
+                        const double gm1 = __fma_rn(rd, gr, -(h * h) * gr1);  // g_{r-1}
+                        gv[4 * u] = lo32(gm1);
+                        gv[4 * u + 1] = hi32(gm1);
+                        gv[4 * u + 2] = lo32(gr);
+                        gv[4 * u + 3] = hi32(gr);
+                    }
+                    av[4 * u] = lo32(acc.x);
+                    av[4 * u + 1] = hi32(acc.x);
+                    av[4 * u + 2] = lo32(acc.y);
+                    av[4 * u + 3] = hi32(acc.y);
+                }
+                tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+                if constexpr (!UNIFORM) tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+            }
+            tm_wait_st();
+            tm_fence_before();
+            if (i < last) nbar_arrive(BAR_H + grp, 2 * G);  // hand off step i+1
+            else nbar_arrive(BAR_E, 2 * G);                   // unit's last update done
+        }
+        // unit boundary.  The group that did not do the last update transforms the
+        // next unit's first row first (its first step), then joins.
+        pre = false;
+        if (grp != lastgrp) {
+            if (has_next) {
+                fft_row(Y + y_index(last, N, p.log_n2, row, 0));
+                pre = true;
+            }
+            nbar_sync(BAR_E, 2 * G);
+            tm_fence_after();
+        }
+        for (int k = grp; k < nch; k += 2) epi_chunk(ucb, ucnt, k);
+        if (has_next) {
+            for (int k = grp; k < nchunks(cnt); k += 2) init_chunk(cb, cnt, k);
+            tm_wait_st();
+            tm_fence_before();
+            nbar_sync(BAR_U, 2 * G);  // next unit's samples set up by both groups
+            tm_fence_after();
+        }
+        S0 += nt;
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
 }
 
 // ------------------------------------------------------------------ launch
@@ -1187,17 +1490,26 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
 //   3: as 2, staged                                 3.81
 //   4: one FFT group, TMEM sample metadata, 3 bufs  3.37
 //   5: two FFT groups, TMEM sample state, Bessel
-//      backward recurrence (L2 >= 2048) [default]   3.05
+//      backward recurrence (L2 >= 2048)             3.05 (2.71 with the 2l FFT)
+//   6: fused samples (L2 = 4096, k2_pass2_fs; others fall back to 5) [default]
 inline int pass2_variant() {
     static const int v = [] {
         const char* e = getenv("NUFFT_PASS2_VARIANT");
-        return e ? atoi(e) : 5;
+        return e ? atoi(e) : 6;
     }();
     return v;
 }
 
 // NUFFT_PASS2_FFT2L=0 selects the three-stage block FFT in the default pass-2
 // kernel (A/B switch for the two-level FFT)
+// NUFFT_PASS2_CONT=1: continuous steps in variant 5 (measured slower: 2.89 vs 2.71 ms, ptxas spills)
+inline bool pass2_cont() {
+    static const bool v = [] {
+        const char* e = getenv("NUFFT_PASS2_CONT");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return v;
+}
 inline bool pass2_fft2l() {
     static const bool v = [] {
         const char* e = getenv("NUFFT_PASS2_FFT2L");
@@ -1224,12 +1536,24 @@ void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1,
     constexpr int threads = G2Shape<L2, SWG>::ALL;
     auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG> : k2_pass2_g2<L2, UNIFORM, false, SWG>;
     if constexpr (L2 == 4096) {
-        if (pass2_fft2l())
+        if (pass2_fft2l() && pass2_cont())
+            fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG, true, true> : k2_pass2_g2<L2, UNIFORM, false, SWG, true, true>;
+        else if (pass2_fft2l())
             fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG, true> : k2_pass2_g2<L2, UNIFORM, false, SWG, true>;
     }
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);
+    NB_LAUNCH();
+}
+
+template <bool UNIFORM>
+void launch_fs(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    constexpr size_t SM = FsShape::SMEM;
+    auto fn = p.ds ? k2_pass2_fs<UNIFORM, true> : k2_pass2_fs<UNIFORM, false>;
+    set_smem(fn, SM);
+    const int grid = (int)std::min<long long>(n1, (long long)sms);
+    fn<<<grid, 2 * FsShape::G, SM, s>>>(Y, f, p);
     NB_LAUNCH();
 }
 
@@ -1283,6 +1607,12 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
                       : launch_ws<L2, false, 3, true>(Y, f, p, n1, ctx.sms, s); break;
             case 4: u ? launch_tm<L2, true>(Y, f, p, n1, ctx.sms, s)
                       : launch_tm<L2, false>(Y, f, p, n1, ctx.sms, s); break;
+            case 6:
+                if constexpr (L2 == 4096) {
+                    u ? launch_fs<true>(Y, f, p, n1, ctx.sms, s) : launch_fs<false>(Y, f, p, n1, ctx.sms, s);
+                    break;
+                }
+                [[fallthrough]];
             case 5:
                 if constexpr (L2 >= 2048) {
                     u ? launch_g2<L2, true>(Y, f, p, n1, ctx.sms, s) : launch_g2<L2, false>(Y, f, p, n1, ctx.sms, s);
