@@ -1170,12 +1170,13 @@ struct FsShape {
 
 // load one Y row (stride-2 layout, y_index), transform it and leave X_r in
 // place in the group's buffer (fft2l_slot order)
-template <class Bar>
-__device__ __forceinline__ void fs_fft_row(const double2* row_in, double2* buf, int tid, const Twiddles<4096>& T,
-                                           Bar gsync) {
-    double2 v[16];
+__device__ __forceinline__ void fs_load_row(double2 (&v)[16], const double2* row_in, int tid) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * 256));
+}
+template <class Bar>
+__device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
+                                            Bar gsync) {
     gsync();  // the group's gathers from its buffer (its previous step) are done
     block_fft_2l<-1>(v, buf, tid, T, gsync);
 #pragma unroll
@@ -1211,87 +1212,126 @@ __global__ void __launch_bounds__(512, 1)
     const double dn = (double)p.n;
 
     // per-sample state of chunk k (slots CH k .. CH k + CH - 1) of a unit
-    auto init_chunk = [&](int cb, int cnt, int k) {
-        unsigned av[4 * CH], hv[2 * CH], dv[2 * CH], t2v[CH];
-        double h[CH];
+    // per-sample state of this group's chunks k = grp, grp + 2, ... of a unit
+    // (slots CH k .. CH k + CH - 1); all global loads are issued first
+    constexpr int KMAX = (W::SLOTS / CH + 1) / 2;  // chunks per group
+    auto init_half = [&](int cb, int cnt) {
+        double dsrc[KMAX * CH];
+        unsigned ksrc[KMAX * CH];
 #pragma unroll
-        for (int u = 0; u < CH; ++u) {
-            const int i = tid + (CH * k + u) * G;
-            double d = 0.0;
-            int t2 = 0;
-            if (i < cnt) {
-                if constexpr (DSRC) {  // type-I core: stored delta and key
-                    d = p.ds[cb + i];
-                    t2 = (int)(p.skey[cb + i] & ((1u << p.log_n2) - 1u));
-                } else {
-                    const double x = p.xs[cb + i];
-                    const double pr = __dmul_rn(dn, x);
-                    const long long sj = (long long)round(pr);
-                    d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
-                    t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
-                }
-            }
-            h[u] = half_phase(d);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
-            hv[2 * u] = lo32(h[u]);
-            hv[2 * u + 1] = hi32(h[u]);
-            dv[2 * u] = lo32(d);
-            dv[2 * u + 1] = hi32(d);
-            t2v[u] = (unsigned)fft2l_slot_of(t2);
-        }
-        tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
-        tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
-        tm_stn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
-        tm_stn<CH>(tl + W::COL_T + CH * k, t2v);
-        if constexpr (!UNIFORM) {
-            // (g_{r1-1}, g_{r1}) by the series; lower orders by the backward recurrence
-            double w[CH], ga[CH], gb[CH];
-#pragma unroll
-            for (int u = 0; u < CH; ++u) w[u] = h[u] * h[u];
-            series_deg<CH>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms, p.deg_rel0);
-            series_deg<CH>(gb, w, kBes + p.r1 * kSeriesTerms, p.deg_rel1);
-            unsigned gv[4 * CH];
+        for (int kk = 0; kk < KMAX; ++kk)
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
-                gv[4 * u] = lo32(ga[u]);
-                gv[4 * u + 1] = hi32(ga[u]);
-                gv[4 * u + 2] = lo32(gb[u]);
-                gv[4 * u + 3] = hi32(gb[u]);
-            }
-            tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
-        }
-    };
-    // f[perm] = 2 exp(2ih) (ih)^r0 acc for chunk k
-    auto epi_chunk = [&](int cb, int cnt, int k) {
-        unsigned av[4 * CH], hv[2 * CH], dv[2 * CH];
-        tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
-        tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
-        tm_ldn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
-        tm_wait_ld();
-#pragma unroll
-        for (int u = 0; u < CH; ++u) {
-            const int i = tid + (CH * k + u) * G;
-            if (i >= cnt) continue;
-            double2 out = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
-            if constexpr (!UNIFORM) {
-                const double h = mk64(hv[2 * u], hv[2 * u + 1]);
-                if (p.r0 > 0) {
-                    double hr = 1.0;
-                    for (int m = 0; m < p.r0; ++m) hr *= h;
-                    out = cscale(out, hr);
-                    switch (p.r0 & 3) {
-                        case 1: out = make_double2(-out.y, out.x); break;
-                        case 2: out = make_double2(-out.x, -out.y); break;
-                        case 3: out = make_double2(out.y, -out.x); break;
-                        default: break;
+                const int i = tid + (CH * (grp + 2 * kk) + u) * G;
+                dsrc[CH * kk + u] = 0.0;
+                ksrc[CH * kk + u] = 0u;
+                if (i < cnt) {
+                    if constexpr (DSRC) {
+                        dsrc[CH * kk + u] = p.ds[cb + i];
+                        ksrc[CH * kk + u] = p.skey[cb + i];
+                    } else {
+                        dsrc[CH * kk + u] = p.xs[cb + i];
                     }
                 }
-                double sn, cs;  // exp(2ih) = exp(-i pi delta), argument exact
-                sincospi(-mk64(dv[2 * u], dv[2 * u + 1]), &sn, &cs);
-                out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
             }
-            __stcs(f + p.perm[cb + i], out);
+#pragma unroll
+        for (int kk = 0; kk < KMAX; ++kk) {
+            const int k = grp + 2 * kk;
+            if (CH * k * G >= cnt) break;
+            unsigned av[4 * CH], hv[2 * CH], dv[2 * CH], t2v[CH];
+            double h[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int i = tid + (CH * k + u) * G;
+                double d = 0.0;
+                int t2 = 0;
+                if (i < cnt) {
+                    if constexpr (DSRC) {  // type-I core: stored delta and key
+                        d = dsrc[CH * kk + u];
+                        t2 = (int)(ksrc[CH * kk + u] & ((1u << p.log_n2) - 1u));
+                    } else {
+                        const double x = dsrc[CH * kk + u];
+                        const double pr = __dmul_rn(dn, x);
+                        const long long sj = (long long)round(pr);
+                        d = __dadd_rn(__dsub_rn(pr, (double)sj), __fma_rn(dn, x, -pr));
+                        t2 = (int)((sj & (p.n - 1)) >> p.log_n1);
+                    }
+                }
+                h[u] = half_phase(d);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) av[4 * u + c] = 0u;
+                hv[2 * u] = lo32(h[u]);
+                hv[2 * u + 1] = hi32(h[u]);
+                dv[2 * u] = lo32(d);
+                dv[2 * u + 1] = hi32(d);
+                t2v[u] = (unsigned)fft2l_slot_of(t2);
+            }
+            tm_stn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+            tm_stn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+            tm_stn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
+            tm_stn<CH>(tl + W::COL_T + CH * k, t2v);
+            if constexpr (!UNIFORM) {
+                // (g_{r1-1}, g_{r1}) by the series; lower orders by the backward recurrence
+                double w[CH], ga[CH], gb[CH];
+#pragma unroll
+                for (int u = 0; u < CH; ++u) w[u] = h[u] * h[u];
+                series_deg<CH>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms, p.deg_rel0);
+                series_deg<CH>(gb, w, kBes + p.r1 * kSeriesTerms, p.deg_rel1);
+                unsigned gv[4 * CH];
+#pragma unroll
+                for (int u = 0; u < CH; ++u) {
+                    gv[4 * u] = lo32(ga[u]);
+                    gv[4 * u + 1] = hi32(ga[u]);
+                    gv[4 * u + 2] = lo32(gb[u]);
+                    gv[4 * u + 3] = hi32(gb[u]);
+                }
+                tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+            }
+        }
+    };
+    // f[perm] = 2 exp(2ih) (ih)^r0 acc for this group's chunks (perm loads first)
+    auto epi_half = [&](int cb, int cnt) {
+        int pm[KMAX * CH];
+#pragma unroll
+        for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int i = tid + (CH * (grp + 2 * kk) + u) * G;
+                pm[CH * kk + u] = i < cnt ? p.perm[cb + i] : 0;
+            }
+#pragma unroll
+        for (int kk = 0; kk < KMAX; ++kk) {
+            const int k = grp + 2 * kk;
+            if (CH * k * G >= cnt) break;
+            unsigned av[4 * CH], hv[2 * CH], dv[2 * CH];
+            tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
+            tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
+            tm_ldn<2 * CH>(tl + W::COL_D + 2 * CH * k, dv);
+            tm_wait_ld();
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int i = tid + (CH * k + u) * G;
+                if (i >= cnt) continue;
+                double2 out = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+                if constexpr (!UNIFORM) {
+                    const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                    if (p.r0 > 0) {
+                        double hr = 1.0;
+                        for (int m = 0; m < p.r0; ++m) hr *= h;
+                        out = cscale(out, hr);
+                        switch (p.r0 & 3) {
+                            case 1: out = make_double2(-out.y, out.x); break;
+                            case 2: out = make_double2(-out.x, -out.y); break;
+                            case 3: out = make_double2(out.y, -out.x); break;
+                            default: break;
+                        }
+                    }
+                    double sn, cs;  // exp(2ih) = exp(-i pi delta), argument exact
+                    sincospi(-mk64(dv[2 * u], dv[2 * u + 1]), &sn, &cs);
+                    out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
+                }
+                __stcs(f + pm[CH * kk + u], out);
+            }
         }
     };
     // set-up and write-out are split between the groups by chunk parity (the
@@ -1317,15 +1357,16 @@ __global__ void __launch_bounds__(512, 1)
     };
     seek(row, -1);
     if (row < n1) {
-        for (int k = grp; k < nchunks(cnt); k += 2) init_chunk(cb, cnt, k);
+        init_half(cb, cnt);
         tm_wait_st();
     }
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    auto fft_row = [&](const double2* row_in) { fs_fft_row(row_in, buf, tid, T, gsync); };
-    int S0 = 0;        // global index of the unit's first step
-    bool pre = false;  // this group's first step of the unit is already transformed
+    int S0 = 0;         // global index of the unit's first step
+    bool pre = false;   // this group's first step of the unit is already transformed
+    bool have = false;  // v holds this group's next row (loaded ahead)
+    double2 v[16];
     while (row < n1) {
         const long long urow = row;
         const int ucb = cb, ucnt = cnt;
@@ -1342,13 +1383,12 @@ __global__ void __launch_bounds__(512, 1)
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
             if (i > 0 || !pre) {
-                if (tid == 0 && i + 2 < nt) {  // warm L2 with this group's next row
-                    const void* nxt = Y + y_index(rr - 2, N, p.log_n2, urow, 0);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
-                                 "r"((unsigned)(2 * L2 * sizeof(double2))) : "memory");
-                }
-                fft_row(Y + y_index(rr, N, p.log_n2, urow, 0));
+                if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
+                fs_fft_regs(v, buf, tid, T, gsync);
             }
+            // this group's next row (step i + 2) is in flight during the update
+            have = i + 2 < nt;
+            if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
             if (i > 0) {  // the other group's update of step i-1 is done
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
                 tm_fence_after();
@@ -1400,15 +1440,16 @@ __global__ void __launch_bounds__(512, 1)
         pre = false;
         if (grp != lastgrp) {
             if (has_next) {
-                fft_row(Y + y_index(last, N, p.log_n2, row, 0));
+                fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
+                fs_fft_regs(v, buf, tid, T, gsync);
                 pre = true;
             }
             nbar_sync(BAR_E, 2 * G);
             tm_fence_after();
         }
-        for (int k = grp; k < nch; k += 2) epi_chunk(ucb, ucnt, k);
+        epi_half(ucb, ucnt);
         if (has_next) {
-            for (int k = grp; k < nchunks(cnt); k += 2) init_chunk(cb, cnt, k);
+            init_half(cb, cnt);
             tm_wait_st();
             tm_fence_before();
             nbar_sync(BAR_U, 2 * G);  // next unit's samples set up by both groups
