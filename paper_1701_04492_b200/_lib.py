@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnufft_b200.so")
+# NUFFT_B200_LIB: load another build of the library (A/B measurements of two builds)
+LIB_PATH = os.environ.get("NUFFT_B200_LIB") or os.path.join(HERE, "libnufft_b200.so")
 
 _sz = C.c_size_t
 _vp = C.c_void_p
