@@ -24,6 +24,9 @@
 // HBM bytes per point (batch 1): c 16 + f 16 + xs/perm 12 + 32 K (Y written
 // and read once) — SURVEY.md §8(d).  No atomics: every f[j] is owned by one
 // thread and sums run in a fixed order, so results are bit-reproducible.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -275,6 +278,153 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     tm_fence_before();
     __syncthreads();
     if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
+// Pass 1 with the Y column stored by the tensor-memory-access engine (TMA)
+// instead of 16 per-thread 16-byte stores: on the LSU path every 32-byte Y
+// sector costs an L1 data-pipe wavefront, and pass 1 ran its L1 pipe at 74 %
+// (2048 of its ~5100 wavefronts per column-term were those stores).  After
+// the two-level FFT each worker writes its twiddled column into its own
+// exchange buffer in the order (b, warp, u, e) — contiguous 512 B per warp
+// store, conflict-free — and one thread issues a single 5-D
+// cp.async.bulk.tensor store of the 64 KiB box, which is exactly that order
+// seen through the Y layout: t1 = e + 2 warp + 16 u + 256 b, dims
+// (e + re/im: 4 doubles, u: 16, warp: 8, 16 rr + b, k2) with strides
+// (-, 8 N2 * 32 B, N2 * 32 B, 128 N2 * 32 B, 32 B) (y_index, N1 = 4096).
+// The next term's exchange waits (wait_group.read) until the engine has read
+// the buffer.
+__global__ void __launch_bounds__(512, 1)
+    k2_pass1_tma(const double2* __restrict__ c, const __grid_constant__ CUtensorMap ymap, Pass1Params p) {
+    constexpr int L1 = 4096, G = 256;
+    extern __shared__ __align__(1024) double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x / G;
+    const int tid = threadIdx.x - grp * G;
+    double2* buf = smem + grp * padded_len(L1);
+    double2* step = smem + 2 * padded_len(L1) + grp * 16;
+    double2* tw = smem + 2 * padded_len(L1) + 32;
+    twiddle_table_build<L1>(tw, threadIdx.x, 2 * G);
+    Twiddles<L1> T;
+    twiddle_init<L1>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 128);
+    const unsigned tc_c = tcol, tc_s = tcol + 64;
+    const int bar = 1 + grp;
+    auto gsync = [bar] { nbar_sync(bar, G); };
+    const long long n2 = 1ll << p.log_n2;
+    const long long N = p.n;
+    const int warp = tid >> 5, e = tid & 1, u = (tid >> 1) & 15;
+    double2* stg = buf + ((warp * 16 + u) * 2 + e);  // + 256 b: staging slot of output b
+    const unsigned buf_s = (unsigned)__cvta_generic_to_shared(buf);
+    for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
+        gsync();  // previous column's readers of step are done
+        for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
+        const int t1_0 = fft2l_out_index(tid, 0);
+        const double2 base = unit_root(k2 * t1_0, N);  // w_N^{k2 t1_0}
+        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            unsigned cv[16], sv[16];
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) {
+                const int q = 4 * j + uu;
+                const double2 x = __ldg(c + (((long long)(tid + q * G)) << p.log_n2) + k2);
+                cv[4 * uu] = lo32(x.x);
+                cv[4 * uu + 1] = hi32(x.x);
+                cv[4 * uu + 2] = lo32(x.y);
+                cv[4 * uu + 3] = hi32(x.y);
+                const double ts = two_s0 + 0.25 * q;
+                double tprev = 1.0, tcur = 0.5 * ts;
+                for (int r = 1; r < p.r0; ++r) {
+                    const double tn = __fma_rn(ts, tcur, -tprev);
+                    tprev = tcur;
+                    tcur = tn;
+                }
+                sv[4 * uu] = lo32(tprev);
+                sv[4 * uu + 1] = hi32(tprev);
+                sv[4 * uu + 2] = lo32(tcur);
+                sv[4 * uu + 3] = hi32(tcur);
+            }
+            tm_st16(tc_c + 16 * j, cv);
+            tm_st16(tc_s + 16 * j, sv);
+        }
+        tm_wait_st();
+        gsync();  // step visible
+        for (int r = p.r0; r < p.r1; ++r) {
+            double2 v[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                unsigned cv[16], sv[16];
+                tm_ld16(tc_c + 16 * j, cv);
+                tm_ld16(tc_s + 16 * j, sv);
+                tm_wait_ld();
+#pragma unroll
+                for (int uu = 0; uu < 4; ++uu) {
+                    const int q = 4 * j + uu;
+                    const double2 x = make_double2(mk64(cv[4 * uu], cv[4 * uu + 1]), mk64(cv[4 * uu + 2], cv[4 * uu + 3]));
+                    const double tprev = mk64(sv[4 * uu], sv[4 * uu + 1]);
+                    const double tcur = mk64(sv[4 * uu + 2], sv[4 * uu + 3]);
+                    const double vr = (r == 0) ? 0.5 : tcur;
+                    v[q] = make_double2(x.x * vr, x.y * vr);
+                    if (r > 0) {  // (T_{r-1}, T_r) -> (T_r, T_{r+1})
+                        const double tn = __fma_rn(two_s0 + 0.25 * q, tcur, -tprev);
+                        sv[4 * uu] = sv[4 * uu + 2];
+                        sv[4 * uu + 1] = sv[4 * uu + 3];
+                        sv[4 * uu + 2] = lo32(tn);
+                        sv[4 * uu + 3] = hi32(tn);
+                    }
+                }
+                if (r > 0) tm_st16(tc_s + 16 * j, sv);
+            }
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // engine done with buf
+            gsync();  // previous term's reads of buf (exchange, TMA) are done
+            block_fft_2l<-1>(v, buf, tid, T, gsync);
+            gsync();  // exchange reads done: buf becomes the staging box
+#pragma unroll
+            for (int b = 0; b < 16; ++b) stg[256 * b] = cmul(v[b], cmul(base, step[b]));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            gsync();  // box complete
+            if (tid == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                        &ymap),
+                    "r"(0), "r"(0), "r"(0), "r"(16 * (r - p.r0)), "r"((int)k2), "r"(buf_s)
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
+        tm_wait_st();
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
+// Y as the 5-D tensor k2_pass1_tma stores into (N1 = 4096, N2 = 2^log_n2)
+bool make_y_tensor_map(CUtensorMap* map, double2* Y, int log_n2, int nterms) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }();
+    if (!encode) return false;
+    const cuuint64_t n2 = 1ull << log_n2;
+    const cuuint64_t row = n2 * 32ull;  // bytes per (t1 >> 1)
+    cuuint64_t dims[5] = {4, 16, 8, 16ull * (cuuint64_t)nterms, n2};
+    cuuint64_t strides[4] = {8 * row, row, 128 * row, 32};
+    cuuint32_t box[5] = {4, 16, 8, 16, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult rc = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Y, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return rc == CUDA_SUCCESS;
 }
 
 // pass 1 for N1 == 1: Y_r[k] = v_r(k) c[k]
@@ -1488,7 +1638,7 @@ int occupancy(const void* fn, int threads, size_t smem) {
 inline int pass1_variant() {
     static const int v = [] {
         const char* e = getenv("NUFFT_PASS1_VARIANT");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 3;
     }();
     return v;
 }
@@ -1503,7 +1653,19 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
             Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
             auto fn = pl.uniform ? k2_pass1_tm<L1, true> : k2_pass1_tm<L1, false>;
             if constexpr (L1 == 4096) {
-                if (pass1_variant() == 2) fn = pl.uniform ? k2_pass1_tm<L1, true, true> : k2_pass1_tm<L1, false, true>;
+                if (pass1_variant() == 3 && !pl.uniform && pl.bk.log_n1 == 12) {
+                    CUtensorMap map;
+                    if (make_y_tensor_map(&map, Y, pl.bk.log_n2, r1 - r0)) {
+                        auto ft = k2_pass1_tma;
+                        set_smem(ft, SMT);
+                        const long long n2 = 1ll << pl.bk.log_n2;
+                        const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
+                        ft<<<grid, 512, SMT, s>>>(c, map, p);
+                        NB_LAUNCH();
+                        return;
+                    }
+                }
+                if (pass1_variant() >= 2) fn = pl.uniform ? k2_pass1_tm<L1, true, true> : k2_pass1_tm<L1, false, true>;
             }
             set_smem(fn, SMT);
             const long long n2 = 1ll << pl.bk.log_n2;
