@@ -1811,9 +1811,14 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
             case 4: u ? launch_tm<L2, true>(Y, f, p, n1, ctx.sms, s)
                       : launch_tm<L2, false>(Y, f, p, n1, ctx.sms, s); break;
             case 6:
+                // (a uniform plan — K = 1, e.g. the size-2N FFTs of the inverse — has one step per
+                // row, so the fused kernel would be all unit boundary: 2.39 vs 1.23 ms per CG
+                // iteration; the warp-specialized kernel overlaps those)
                 if constexpr (L2 == 4096) {
-                    u ? launch_fs<true>(Y, f, p, n1, ctx.sms, s) : launch_fs<false>(Y, f, p, n1, ctx.sms, s);
-                    break;
+                    if (!u) {
+                        launch_fs<false>(Y, f, p, n1, ctx.sms, s);
+                        break;
+                    }
                 }
                 [[fallthrough]];
             case 5:
