@@ -194,3 +194,22 @@ def test_cfg3_error_sweep_vs_gpu_direct(nb):
     want = nb.nudft_direct(idx / N24, w, c)
     rel = np.linalg.norm(f[idx] - want) / np.linalg.norm(want)
     assert rel <= 1e-14, rel
+
+
+def test_cfg3_type1_adjoint_identity(nb):
+    """Type-I adjoint at full size runs the fused-sample pass 2 on the type-I plan
+    (delta and key from the frequencies, k2_pass2_fs<., DSRC>): check it against
+    the transpose core through <A1 c, g> == <c, A1^H g>, and bit-reproducibility."""
+    rng = np.random.default_rng(31)
+    w = np.clip(np.arange(N24) + rng.uniform(-0.5, 0.5, N24), 0, N24)
+    c = rng.standard_normal(N24) + 1j * rng.standard_normal(N24)
+    g = rng.standard_normal(N24) + 1j * rng.standard_normal(N24)
+    p = nb.plan_nufft1(w, 1e-12)
+    f = nb.exec_nufft1(p, c)
+    a1 = nb.exec_nufft1_adjoint(p, g)
+    a2 = nb.exec_nufft1_adjoint(p, g)
+    assert np.array_equal(a1.view(np.float64), a2.view(np.float64))
+    lhs = np.vdot(g, f)
+    rhs = np.vdot(a1, c)
+    scale = np.linalg.norm(g) * np.linalg.norm(f)
+    assert abs(lhs - rhs) <= 1e-13 * scale, (lhs, rhs)
