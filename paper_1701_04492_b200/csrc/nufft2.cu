@@ -1334,6 +1334,20 @@ __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int 
     gsync();  // X complete
 }
 
+// diagnostics: clock64 stamps of CTA 0 (thread 0 of each group, steps < 64) when
+// built with -DNB_FS_TRACE and run with NUFFT_TRACE_PASS2=1 (the predicated stores
+// cost ~10 % of pass 2, so they are compiled out by default)
+#ifdef NB_FS_TRACE
+#define FS_TRACE(step, e)                                                                       \
+    do {                                                                                        \
+        if (p.trace && blockIdx.x == 0 && tid == 0 && (step) < 64) p.trace[8 * (step) + (e)] = clock64(); \
+    } while (0)
+#else
+#define FS_TRACE(step, e) \
+    do {                  \
+    } while (0)
+#endif
+
 template <bool UNIFORM, bool DSRC>
 __global__ void __launch_bounds__(512, 1)
     k2_pass2_fs(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
@@ -1532,10 +1546,12 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = (grp - S0) & 1; i < nt; i += 2) {
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
+            FS_TRACE(S0 + i, 0);
             if (i > 0 || !pre) {
                 if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
             }
+            FS_TRACE(S0 + i, 1);
             // this group's next row (step i + 2) is in flight during the update
             have = i + 2 < nt;
             if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
@@ -1543,6 +1559,7 @@ __global__ void __launch_bounds__(512, 1)
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
                 tm_fence_after();
             }
+            FS_TRACE(S0 + i, 2);
             const double rd = (double)r;
 #pragma unroll 1
             for (int k = 0; k < nch; ++k) {
@@ -1582,6 +1599,7 @@ __global__ void __launch_bounds__(512, 1)
             }
             tm_wait_st();
             tm_fence_before();
+            FS_TRACE(S0 + i, 3);
             if (i < last) nbar_arrive(BAR_H + grp, 2 * G);  // hand off step i+1
             else nbar_arrive(BAR_E, 2 * G);                   // unit's last update done
         }
@@ -1597,9 +1615,12 @@ __global__ void __launch_bounds__(512, 1)
             nbar_sync(BAR_E, 2 * G);
             tm_fence_after();
         }
+        FS_TRACE(S0 + last, 4 + grp);
         epi_half(ucb, ucnt);
+        FS_TRACE(S0 + last + 1, 4 + grp);
         if (has_next) {
             init_half(cb, cnt);
+            FS_TRACE(S0 + last, 6 + grp);
             tm_wait_st();
             tm_fence_before();
             nbar_sync(BAR_U, 2 * G);  // next unit's samples set up by both groups
@@ -1846,6 +1867,13 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
         NB_CUDA(cudaStreamSynchronize(s));
         NB_CUDA(cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost));
         const unsigned long long t0 = h[0];
+        if (pass2_variant() == 6 && L2 == 4096 && !pl.uniform) {  // k2_pass2_fs (-DNB_FS_TRACE build)
+            for (int i = 0; i < 64; ++i)
+                fprintf(stderr, "fs S=%2d grp %d fft[%7lld %7lld] upd[%7lld %7lld] bnd[epi %7lld %7lld init %7lld %7lld]\n", i, i & 1,
+                        (long long)(h[8 * i] - t0), (long long)(h[8 * i + 1] - t0), (long long)(h[8 * i + 2] - t0),
+                        (long long)(h[8 * i + 3] - t0), (long long)(h[8 * i + 4] - t0), (long long)(h[8 * i + 5] - t0),
+                        (long long)(h[8 * i + 6] - t0), (long long)(h[8 * i + 7] - t0));
+        } else
         for (int i = 0; i < r1 - r0; ++i)
             fprintf(stderr, "trace i=%2d fft[start %7lld input %7lld done %7lld]  smp[full %7lld horner %7lld staged %7lld]\n", i,
                     (long long)(h[8 * i] - t0), (long long)(h[8 * i + 1] - t0), (long long)(h[8 * i + 2] - t0),
