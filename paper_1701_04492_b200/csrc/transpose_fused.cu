@@ -26,6 +26,7 @@
 // HBM bytes per point (batch 1): g 16 (gathered) + f 16 + delta/key/perm 16
 // + 32 K (Z written and read once).
 #include <algorithm>
+#include <cstdlib>
 
 #include "bessel.cuh"
 #include "fft_block.cuh"
@@ -480,9 +481,14 @@ __global__ void __launch_bounds__(L1 / 16, 1)
 // tensor memory (tmem.cuh: 128 columns per thread, [acc re/im lo/hi x 16]
 // [T_{r-1}, T_r lo/hi x 16]) instead of 128 registers, and each worker
 // exchanges through one padded buffer of its own (as k2_pass1_tm, nufft2.cu).
-template <int L1, bool UNIFORM>
+// F2L (L1 = 4096): the column FFT is block_fft_2l (two group barriers per term
+// instead of four); the thread's outputs are then k1 = k1_0 + 256 q with
+// k1_0 = fft2l_out_index(tid, 0), so the accumulator slots, the Chebyshev
+// arguments and the final f rows follow k1_0.
+template <int L1, bool UNIFORM, bool F2L = false>
 __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     k1_passB_tm(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p) {
+    static_assert(!F2L || L1 == 4096, "two-level FFT is 4096-point");
     constexpr int G = L1 / 16;
     extern __shared__ double2 smem[];
     __shared__ unsigned tmem_base;
@@ -510,7 +516,8 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
         gsync();  // previous column's readers of step are done
         for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
         const double2 base = unit_root(k2 * tid, N);                          // w_N^{k2 tid}
-        const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
+        const int k1_0 = F2L ? fft2l_out_index(tid, 0) : tid;                 // first output row
+        const double two_s0 = (double)(4 * ((((long long)k1_0) << p.log_n2) + k2)) / (double)N - 2.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {  // acc = 0, state (T_{r0-1}, T_r0)
             unsigned av[16], sv[16];
@@ -544,7 +551,11 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 v[q] = cmul(__ldcg(col + (t1 << p.log_n2)), cmul(base, step[q]));
             }
             gsync();  // previous term's last-stage reads of buf are done
-            block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+            if constexpr (F2L) {
+                block_fft_2l<-1>(v, buf, tid, T, gsync);
+            } else {
+                block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 unsigned av[16], sv[16];
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             tm_wait_ld();
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const long long k1 = tid + (4 * j + u) * G;
+                const long long k1 = k1_0 + (4 * j + u) * G;
                 f[(k1 << p.log_n2) + k2] =
                     make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
             }
@@ -684,6 +695,10 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         constexpr size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
         PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
+        if constexpr (L1 == 4096) {
+            static const bool f2l = !getenv("NUFFT_PASSB_FFT3");  // A/B: three-stage FFT
+            if (f2l) fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
+        }
         set_smem(fn, SMT);
         const long long n2 = 1ll << pl.bk.log_n2;
         const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
