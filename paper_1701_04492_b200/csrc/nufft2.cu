@@ -1439,8 +1439,29 @@ __global__ void __launch_bounds__(512, 1)
                 double w[CH], ga[CH], gb[CH];
 #pragma unroll
                 for (int u = 0; u < CH; ++u) w[u] = h[u] * h[u];
-                series_deg<CH>(ga, w, kBes + (p.r1 - 1) * kSeriesTerms, p.deg_rel0);
-                series_deg<CH>(gb, w, kBes + p.r1 * kSeriesTerms, p.deg_rel1);
+                // rolled Horner (uniform degree; same operations as series_fixed): this code
+                // runs once per unit, and the unrolled switch made it ~10x larger
+                {
+                    const double* a0 = kBes + (p.r1 - 1) * kSeriesTerms;
+                    const double* a1 = kBes + p.r1 * kSeriesTerms;
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) {
+                        ga[u] = a0[p.deg_rel0];
+                        gb[u] = a1[p.deg_rel1];
+                    }
+#pragma unroll 1
+                    for (int m = p.deg_rel0 - 1; m >= 0; --m) {
+                        const double am = a0[m];
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) ga[u] = __fma_rn(ga[u], w[u], am);
+                    }
+#pragma unroll 1
+                    for (int m = p.deg_rel1 - 1; m >= 0; --m) {
+                        const double am = a1[m];
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) gb[u] = __fma_rn(gb[u], w[u], am);
+                    }
+                }
                 unsigned gv[4 * CH];
 #pragma unroll
                 for (int u = 0; u < CH; ++u) {
