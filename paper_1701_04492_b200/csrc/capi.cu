@@ -479,12 +479,60 @@ int nufft_plan2_exec(const nufft_plan2* plan, const double* c_dev, double* f_dev
                      void* stream) {
     return nufft_plan2_exec_terms(plan, c_dev, f_dev, batch, 0, plan->core.K, stream);
 }
+// batch > 1: the vectors stream through two device slots on three streams so the
+// host->device copy of c_{b+1} and the device->host copy of f_{b-1} overlap the
+// transform of vector b (the PCIe copies of one 2^24 vector take longer than its
+// transform).  Results are identical to the one-shot path (same kernels per vector).
+static void plan2_host_pipelined(const nb::CorePlan& p, const double* c, double* f, size_t batch) {
+    const size_t nd = 2 * p.n;  // doubles per vector
+    cudaStream_t s0 = cudaStreamPerThread;
+    cudaStream_t st[3];
+    cudaEvent_t ev[3][2];
+    for (auto& x : st) NB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto& e : ev)
+        for (auto& x : e) NB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    {
+        nb::DevBuf din(8 * nd * 2, s0), dout(8 * nd * 2, s0);
+        cudaEvent_t ready;
+        NB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        NB_CUDA(cudaEventRecord(ready, s0));
+        for (auto& x : st) NB_CUDA(cudaStreamWaitEvent(x, ready, 0));
+        enum { H2D = 0, COMP = 1, D2H = 2 };
+        for (size_t b = 0; b < batch; ++b) {
+            const int slot = (int)(b & 1);
+            double* a = din.as<double>() + nd * slot;
+            double* o = dout.as<double>() + nd * slot;
+            if (b >= 2) NB_CUDA(cudaStreamWaitEvent(st[H2D], ev[COMP][slot], 0));  // din[slot] consumed
+            NB_CUDA(cudaMemcpyAsync(a, c + nd * b, 8 * nd, cudaMemcpyHostToDevice, st[H2D]));
+            NB_CUDA(cudaEventRecord(ev[H2D][slot], st[H2D]));
+            NB_CUDA(cudaStreamWaitEvent(st[COMP], ev[H2D][slot], 0));
+            if (b >= 2) NB_CUDA(cudaStreamWaitEvent(st[COMP], ev[D2H][slot], 0));  // dout[slot] drained
+            nb::exec_type2(p, reinterpret_cast<const double2*>(a), reinterpret_cast<double2*>(o), 1, 0, p.K,
+                           st[COMP]);
+            NB_CUDA(cudaEventRecord(ev[COMP][slot], st[COMP]));
+            NB_CUDA(cudaStreamWaitEvent(st[D2H], ev[COMP][slot], 0));
+            NB_CUDA(cudaMemcpyAsync(f + nd * b, o, 8 * nd, cudaMemcpyDeviceToHost, st[D2H]));
+            NB_CUDA(cudaEventRecord(ev[D2H][slot], st[D2H]));
+        }
+        for (auto& x : st) NB_CUDA(cudaStreamSynchronize(x));
+        NB_CUDA(cudaEventDestroy(ready));
+    }
+    NB_CUDA(cudaStreamSynchronize(s0));
+    for (auto& e : ev)
+        for (auto& x : e) NB_CUDA(cudaEventDestroy(x));
+    for (auto& x : st) NB_CUDA(cudaStreamDestroy(x));
+    nb::fft_count(p.n, p.K * batch);
+}
 int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, double* f,
                           size_t batch) {
     return guard([&] {
         const nb::CorePlan& p = plan->core;
         if (len != p.n) nb::throw_invalid("exec_nufft2: length mismatch");
         NB_CUDA(cudaSetDevice(p.device));
+        if (batch > 1) {
+            plan2_host_pipelined(p, c, f, batch);
+            return;
+        }
         cudaStream_t s = cudaStreamPerThread;
         host_roundtrip(c, 2 * p.n * batch, f, 2 * p.n * batch, s, [&](double2* a, double2* b) {
             nb::exec_type2(p, a, b, batch, 0, p.K, s);

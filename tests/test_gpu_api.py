@@ -211,3 +211,22 @@ def test_batched_exec_equals_singles_all_types(nb):
         pd.execute_device(Cs[b].data_ptr(), fs.data_ptr(), 1)
         torch.cuda.synchronize()
         assert torch.equal(torch.view_as_real(fs), torch.view_as_real(fb[b]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("logn", [14, 24])
+def test_type2_host_batch_pipelined_equals_singles(nb, logn):
+    """exec_host with batch > 1 streams the vectors through two device slots on three
+    streams (H2D / transform / D2H overlapped): results must be bit-identical to
+    one host call per vector, including the slot reuse from the third vector on."""
+    n = 1 << logn
+    rng = np.random.default_rng(41 + logn)
+    p = nb.plan_nufft2(rng.random(n), 1e-14)
+    batch = 5 if logn < 20 else 3
+    c = (rng.standard_normal((batch, n)) + 1j * rng.standard_normal((batch, n))).astype(np.complex128)
+    f = np.empty_like(c)
+    p.execute_host_ptr(c.ctypes.data, f.ctypes.data, batch)
+    for b in range(batch):
+        fb = np.empty(n, dtype=np.complex128)
+        p.execute_host_ptr(c[b].ctypes.data, fb.ctypes.data, 1)
+        assert np.array_equal(f[b].view(np.float64), fb.view(np.float64)), b
