@@ -17,6 +17,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I" + os.path.join(HERE, "..", "include")]
+# NB_NVCC_EXTRA: extra nvcc flags for experiment builds (e.g. "-DNB_FS_TRACE")
+FLAGS += os.environ.get("NB_NVCC_EXTRA", "").split()
 
 
 def _sources():
