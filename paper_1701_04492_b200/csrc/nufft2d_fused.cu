@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(LM / 16, 1)
             for (int i = tid; i < CAP; i += G) {
                 const bool ok = i < cnt;
                 shy[i] = (ok && !p.uy_uniform) ? half_phase(p.dys[cb + i]) : 0.0;
-                sty[i] = ok ? p.tys[cb + i] : (unsigned short)0;
+                // gather slot of X[ty]: natural index, or its place after the two-level FFT
+                sty[i] = ok ? (unsigned short)(LM == 4096 ? fft2l_slot_of(p.tys[cb + i]) : p.tys[cb + i])
+                            : (unsigned short)0;
             }
             for (int r1 = p.kx - 1; r1 >= 0; --r1) {
                 __syncthreads();  // previous term's gathers from buf / reads of rcol done
@@ -169,10 +171,16 @@ __global__ void __launch_bounds__(LM / 16, 1)
                     __syncthreads();  // rcol visible; previous gathers from buf done
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
-                    block_fft_1buf<LM, -1>(v, buf, tid, T, [] { __syncthreads(); });
-                    __syncthreads();  // last-stage reads of buf done
+                    if constexpr (LM == 4096) {  // two-level FFT, X left in place (fft2l_slot)
+                        block_fft_2l<-1>(v, buf, tid, T, [] { __syncthreads(); });
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                        for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
+                    } else {
+                        block_fft_1buf<LM, -1>(v, buf, tid, T, [] { __syncthreads(); });
+                        __syncthreads();  // last-stage reads of buf done
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
+                    }
                     __syncthreads();
                     // S <- S (i hy) + gy_r2(hy^2) X[ty]
                     const double* a = kBes + r2 * kSeriesTerms;

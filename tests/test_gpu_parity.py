@@ -196,9 +196,10 @@ def test_type2d_vs_oracle(nb, port, m, n, cnt):
     check(nb.exec_nufft2d2(pg, C2), po.execute(C2), 1e-9)
 
 
-@pytest.mark.parametrize("m,n,cnt", [(16, 16, 300), (256, 128, 20000), (128, 512, 40000)])
+@pytest.mark.parametrize("m,n,cnt", [(16, 16, 300), (256, 128, 20000), (128, 512, 40000), (4096, 16, 30000)])
 def test_type2d_fused_vs_oracle(nb, port, m, n, cnt):
-    """Power-of-two grids take the fused row/column kernels."""
+    """Power-of-two grids take the fused row/column kernels (m = 4096: the column
+    kernel's two-level FFT with X gathered from its in-place slots)."""
     rng = port.sampler(900 + m + n)
     x = rng.uniform_vector(cnt, 0.0, 1.0)
     y = rng.uniform_vector(cnt, 0.0, 1.0)
