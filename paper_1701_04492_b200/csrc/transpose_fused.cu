@@ -222,9 +222,12 @@ struct PassATmShape {
     static_assert((2 * G / 32 + 3) / 4 * 6 * QA <= 512, "TMEM columns");
 };
 
-template <int L2, bool UNIFORM>
+// F2L (L2 = 4096): the row FFT is block_fft_2l; output k2 of register q is
+// fft2l_out_index(tid, q) (lanes 2i, 2i+1 write adjacent k2: full 32-byte sectors).
+template <int L2, bool UNIFORM, bool F2L = false>
 __global__ void __launch_bounds__(2 * (L2 / 16), 1)
     k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p) {
+    static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
     using S = PassATmShape<L2>;
     constexpr int G = S::G;
     constexpr int QA = S::QA;
@@ -379,12 +382,16 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
                     v[q] = acc;
                 }
                 gsync();  // terms read before stage 1 reuses buf
-                block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                if constexpr (F2L) {
+                    block_fft_2l<-1>(v, buf, tid, T, gsync);
+                } else {
+                    block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                }
                 double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     const double2 z = UNIFORM ? v[q] : rot_ipow(v[q], r);
-                    const int k2 = tid + q * G;
+                    const int k2 = F2L ? fft2l_out_index(tid, q) : tid + q * G;
                     out[k2] = chunk == 0 ? z : cadd(out[k2], z);
                 }
             }
@@ -673,6 +680,8 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
     if constexpr (L2 == 4096) {  // at 2048 two single-worker CTAs per SM are as good
         constexpr size_t SMT = PassATmShape<L2>::SMEM;
         auto fnt = pl.uniform ? k1_passA_tm<L2, true> : k1_passA_tm<L2, false>;
+        static const bool f2l = !getenv("NUFFT_PASSA_FFT3");  // A/B: three-stage FFT
+        if (f2l) fnt = pl.uniform ? k1_passA_tm<L2, true, true> : k1_passA_tm<L2, false, true>;
         set_smem(fnt, SMT);
         const long long rows = 1ll << pl.bk.log_n1;
         const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
