@@ -25,6 +25,9 @@
 //
 // HBM bytes per point (batch 1): g 16 (gathered) + f 16 + delta/key/perm 16
 // + 32 K (Z written and read once).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -224,15 +227,21 @@ struct PassATmShape {
 
 // F2L (L2 = 4096): the row FFT is block_fft_2l; output k2 of register q is
 // fft2l_out_index(tid, q) (lanes 2i, 2i+1 write adjacent k2: full 32-byte sectors).
-template <int L2, bool UNIFORM, bool F2L = false>
+// TMA (with F2L): a single-chunk row term leaves through the tensor-memory-access
+// engine — the z values are staged conflict-free in the exchange buffer in the
+// order (b, warp, u, e) and one 5-D cp.async.bulk.tensor store writes the 64 KiB
+// Z row (dims: e pair = 4 doubles, u, warp, b, rr N1 + row), as in k2_pass1_tma.
+template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false>
 __global__ void __launch_bounds__(2 * (L2 / 16), 1)
-    k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p) {
+    k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p,
+                const __grid_constant__ CUtensorMap zmap) {
     static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
+    static_assert(!TMA || F2L, "TMA store needs the two-level output order");
     using S = PassATmShape<L2>;
     constexpr int G = S::G;
     constexpr int QA = S::QA;
     constexpr int CAP = S::CAP;
-    extern __shared__ double2 smem[];
+    extern __shared__ __align__(1024) double2 smem[];  // TMA box source: 128-byte aligned
     __shared__ unsigned tmem_base;
     const int grp = threadIdx.x / G;
     const int tid = threadIdx.x - grp * G;
@@ -265,6 +274,7 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
         }
         for (int cb = beg, chunk = 0; cb < end; cb += CAP, ++chunk) {
             const int cnt = min(CAP, end - cb);
+            if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             gsync();  // previous chunk's readers of bo / buf are done
             for (int i = tid; i < L2; i += G) bo[i] = 0u;
             gsync();
@@ -313,7 +323,8 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
             }
             tm_wait_st();
             for (int r = p.r0; r < p.r1; ++r) {
-                gsync();  // previous term's last-stage reads of buf are done
+                if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                gsync();  // previous term's last-stage reads of buf (and the TMA's) are done
                 // term phase: buf[i] = g_r(h_i^2) Q_i, then Q_i <- h_i Q_i
                 const double* a = kBes + r * kSeriesTerms;
                 const int deg = p.deg[r];
@@ -388,16 +399,35 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
                     block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                 }
                 double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
+                if (TMA && chunk == 0) {
+                    gsync();  // exchange reads done: buf becomes the staging box
+                    double2* stg = buf + (((tid >> 5) * 16 + ((tid >> 1) & 15)) * 2 + (tid & 1));
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const double2 z = UNIFORM ? v[q] : rot_ipow(v[q], r);
-                    const int k2 = F2L ? fft2l_out_index(tid, q) : tid + q * G;
-                    out[k2] = chunk == 0 ? z : cadd(out[k2], z);
+                    for (int q = 0; q < 16; ++q) stg[256 * q] = UNIFORM ? v[q] : rot_ipow(v[q], r);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    gsync();  // box complete
+                    if (tid == 0) {
+                        const int z4 = (int)(((long long)(r - p.r0) << p.log_n1) + row);
+                        asm volatile(
+                            "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                                &zmap),
+                            "r"(0), "r"(0), "r"(0), "r"(0), "r"(z4), "r"((unsigned)__cvta_generic_to_shared(buf))
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const double2 z = UNIFORM ? v[q] : rot_ipow(v[q], r);
+                        const int k2 = F2L ? fft2l_out_index(tid, q) : tid + q * G;
+                        out[k2] = chunk == 0 ? z : cadd(out[k2], z);
+                    }
                 }
             }
             tm_wait_st();
         }
     }
+    if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tm_fence_before();
     __syncthreads();
     if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
@@ -651,6 +681,27 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
     f[k] = acc;
 }
 
+// Z (row-major rr*N + row*4096 + k2) as the 5-D tensor k1_passA_tm<.., TMA> stores into
+bool make_z_tensor_map(CUtensorMap* map, double2* Z, int log_n1, int nterms) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }();
+    if (!encode) return false;
+    const cuuint64_t rows = (cuuint64_t)nterms << log_n1;
+    cuuint64_t dims[5] = {4, 16, 8, 16, rows};
+    cuuint64_t strides[4] = {256, 32, 4096, 65536};  // bytes: u, warp, b, (rr, row)
+    cuuint32_t box[5] = {4, 16, 8, 16, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Z, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class F>
 void set_smem(F* fn, size_t bytes) {
     NB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -681,11 +732,17 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
         constexpr size_t SMT = PassATmShape<L2>::SMEM;
         auto fnt = pl.uniform ? k1_passA_tm<L2, true> : k1_passA_tm<L2, false>;
         static const bool f2l = !getenv("NUFFT_PASSA_FFT3");  // A/B: three-stage FFT
+        static const bool tma = !getenv("NUFFT_PASSA_NO_TMA");  // A/B: LSU row stores
+        CUtensorMap zmap{};
         if (f2l) fnt = pl.uniform ? k1_passA_tm<L2, true, true> : k1_passA_tm<L2, false, true>;
+        if constexpr (L2 == 4096) {
+            if (f2l && tma && make_z_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
+                fnt = pl.uniform ? k1_passA_tm<L2, true, true, true> : k1_passA_tm<L2, false, true, true>;
+        }
         set_smem(fnt, SMT);
         const long long rows = 1ll << pl.bk.log_n1;
         const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
-        fnt<<<gridt, 2 * (L2 / 16), SMT, s>>>(g, Z, p);
+        fnt<<<gridt, 2 * (L2 / 16), SMT, s>>>(g, Z, p, zmap);
         NB_LAUNCH();
         return;
     }
