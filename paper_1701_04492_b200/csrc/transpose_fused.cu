@@ -522,13 +522,21 @@ __global__ void __launch_bounds__(L1 / 16, 1)
 // instead of four); the thread's outputs are then k1 = k1_0 + 256 q with
 // k1_0 = fft2l_out_index(tid, 0), so the accumulator slots, the Chebyshev
 // arguments and the final f rows follow k1_0.
-template <int L1, bool UNIFORM, bool F2L = false>
+// TMA (with F2L): the Z column of each term is loaded by one 5-D
+// cp.async.bulk.tensor load (4096 x 16 B, natural t1 order) into the worker's
+// exchange buffer, issued as soon as the previous term's FFT has released the
+// buffer so it overlaps the accumulator update; the FFT inputs then come from
+// contiguous shared memory instead of 16 scattered global loads per thread.
+template <int L1, bool UNIFORM, bool F2L = false, bool TMA = false>
 __global__ void __launch_bounds__(2 * (L1 / 16), 1)
-    k1_passB_tm(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p) {
+    k1_passB_tm(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p,
+                const __grid_constant__ CUtensorMap zmap) {
     static_assert(!F2L || L1 == 4096, "two-level FFT is 4096-point");
+    static_assert(!TMA || F2L, "TMA load path is for the two-level kernel");
     constexpr int G = L1 / 16;
-    extern __shared__ double2 smem[];
+    extern __shared__ __align__(1024) double2 smem[];
     __shared__ unsigned tmem_base;
+    __shared__ __align__(8) unsigned long long colbar[2];  // per worker: column landed
     const int grp = threadIdx.x / G;
     const int tid = threadIdx.x - grp * G;
     double2* buf = smem + grp * padded_len(L1);
@@ -538,11 +546,27 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     Twiddles<L1> T;
     twiddle_init<L1>(T, tw, tid);
     if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    if (TMA && tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&colbar[grp]))
+                     : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
     const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 128);
     const unsigned tc_a = tcol, tc_s = tcol + 64;
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(&colbar[grp]);
+    const unsigned buf_s = (unsigned)__cvta_generic_to_shared(smem + grp * padded_len(L1));
+    int col_phase = 0;
+    auto col_load = [&](int rr, long long kk2) {  // thread 0 of the worker
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(65536) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+            "%6}], [%7];" ::"r"(buf_s),
+            "l"(&zmap), "r"(0), "r"(0), "r"(0), "r"(rr), "r"((int)kk2), "r"(bar_s)
+            : "memory");
+    };
     const int bar = 1 + grp;
     auto gsync = [bar] {
         asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory");
@@ -578,20 +602,43 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             if constexpr (!UNIFORM) tm_st16(tc_s + 16 * j, sv);
         }
         tm_wait_st();
+        if constexpr (TMA) {
+            gsync();  // the previous column's last exchange reads of buf are done
+            if (tid == 0) col_load(0, k2);
+        }
         gsync();  // step visible
         for (int r = p.r0; r < p.r1; ++r) {
-            const double2* col = Z + (long long)(r - p.r0) * N + k2;
             double2 v[16];
+            if constexpr (TMA) {
+                asm volatile(
+                    "{\n\t.reg .pred P;\n"
+                    "CBW_%=:\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                    "@!P bra CBW_%=;\n}" ::"r"(bar_s),
+                    "r"(col_phase)
+                    : "memory");
+                col_phase ^= 1;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const long long t1 = tid + q * G;
-                v[q] = cmul(__ldcg(col + (t1 << p.log_n2)), cmul(base, step[q]));
+                for (int q = 0; q < 16; ++q) v[q] = cmul(buf[tid + q * G], cmul(base, step[q]));
+            } else {
+                const double2* col = Z + (long long)(r - p.r0) * N + k2;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const long long t1 = tid + q * G;
+                    v[q] = cmul(__ldcg(col + (t1 << p.log_n2)), cmul(base, step[q]));
+                }
             }
-            gsync();  // previous term's last-stage reads of buf are done
+            gsync();  // previous term's last-stage reads of buf (and this term's inputs) are done
             if constexpr (F2L) {
                 block_fft_2l<-1>(v, buf, tid, T, gsync);
             } else {
                 block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
+            }
+            if constexpr (TMA) {
+                if (r + 1 < p.r1) {
+                    gsync();  // exchange reads done: the next term's column may land in buf
+                    if (tid == 0) col_load(r + 1 - p.r0, k2);
+                }
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -681,6 +728,28 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
     f[k] = acc;
 }
 
+// Z columns (rr*N + t1*4096 + k2, N1 = 2^log_n1 rows) as the 5-D tensor k1_passB_tm<.., TMA>
+// loads from: (re/im, t1 & 255, t1 >> 8, rr, k2), box = one column of one term
+bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int nterms) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }();
+    if (!encode || log_n1 != 12) return false;
+    const cuuint64_t row = 4096ull * 16ull;  // bytes per t1 (N2 = 4096)
+    cuuint64_t dims[5] = {2, 256, 16, (cuuint64_t)nterms, 4096};
+    cuuint64_t strides[4] = {row, 256 * row, 4096 * row, 16};
+    cuuint32_t box[5] = {2, 256, 16, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Z, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Z (row-major rr*N + row*4096 + k2) as the 5-D tensor k1_passA_tm<.., TMA> stores into
 bool make_z_tensor_map(CUtensorMap* map, double2* Z, int log_n1, int nterms) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -761,14 +830,18 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         constexpr size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
         PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
+        CUtensorMap zmap{};
         if constexpr (L1 == 4096) {
             static const bool f2l = !getenv("NUFFT_PASSB_FFT3");  // A/B: three-stage FFT
+            static const bool tma = !getenv("NUFFT_PASSB_NO_TMA");  // A/B: LSU column loads
             if (f2l) fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
+            if (f2l && tma && pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
+                fn = pl.uniform ? k1_passB_tm<L1, true, true, true> : k1_passB_tm<L1, false, true, true>;
         }
         set_smem(fn, SMT);
         const long long n2 = 1ll << pl.bk.log_n2;
         const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
-        fn<<<grid, 2 * (L1 / 16), SMT, s>>>(Z, f, p);
+        fn<<<grid, 2 * (L1 / 16), SMT, s>>>(Z, f, p, zmap);
         NB_LAUNCH();
         return;
     }
