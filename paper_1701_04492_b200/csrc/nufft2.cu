@@ -1794,7 +1794,10 @@ void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1,
 
 template <bool UNIFORM>
 void launch_fs(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
-    constexpr size_t SM = FsShape::SMEM;
+    // NUFFT_FS_EXTRA_SMEM (KiB, diagnostics): launch with more shared memory than needed,
+    // i.e. a smaller L1 carve-out (this kernel is sensitive to it)
+    static const int extra_kb = getenv("NUFFT_FS_EXTRA_SMEM") ? atoi(getenv("NUFFT_FS_EXTRA_SMEM")) : 0;
+    const size_t SM = std::min<size_t>(227 * 1024, FsShape::SMEM + 1024 * (size_t)extra_kb);
     auto fn = p.ds ? k2_pass2_fs<UNIFORM, true> : k2_pass2_fs<UNIFORM, false>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms);
