@@ -359,7 +359,16 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
 #pragma unroll
                         for (int u = 0; u < 4; ++u) gr[u] = 1.0;
                     } else {
-                        series_deg<4>(gr, w, a, deg);
+                        // rolled Horner (uniform degree; the same operations as series_fixed):
+                        // the switch-unrolled form multiplied the kernel's code size
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) gr[u] = a[deg];
+#pragma unroll 1
+                        for (int m = deg - 1; m >= 0; --m) {
+                            const double am = a[m];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
+                        }
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
