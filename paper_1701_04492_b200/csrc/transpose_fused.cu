@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     constexpr int G = L1 / 16;
     extern __shared__ __align__(1024) double2 smem[];
     __shared__ unsigned tmem_base;
-    __shared__ __align__(8) unsigned long long colbar[2];  // per worker: column landed
+    __shared__ __align__(8) unsigned long long colbar[4];  // per worker: [2 grp] first half, [2 grp + 1] second half
     const int grp = threadIdx.x / G;
     const int tid = threadIdx.x - grp * G;
     double2* buf = smem + grp * padded_len(L1);
@@ -556,8 +556,10 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     twiddle_init<L1>(T, tw, tid);
     if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
     if (TMA && tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&colbar[grp]))
-                     : "memory");
+        for (int h = 0; h < 2; ++h)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&colbar[2 * grp + h]))
+                         : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tm_fence_before();
@@ -565,15 +567,31 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     tm_fence_after();
     const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((threadIdx.x >> 7) * 128);
     const unsigned tc_a = tcol, tc_s = tcol + 64;
-    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(&colbar[grp]);
+    // the column of a term arrives in two 32 KiB halves: t1 < 2048 into a dedicated
+    // buffer `pre` (issued a whole term ahead), t1 >= 2048 into the exchange buffer
+    // (issued once the previous FFT has released it)
+    double2* pre = smem + 2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN + grp * 2048;
+    const unsigned bar_s0 = (unsigned)__cvta_generic_to_shared(&colbar[2 * grp]);
+    const unsigned bar_s1 = (unsigned)__cvta_generic_to_shared(&colbar[2 * grp + 1]);
     const unsigned buf_s = (unsigned)__cvta_generic_to_shared(smem + grp * padded_len(L1));
+    const unsigned pre_s = (unsigned)__cvta_generic_to_shared(pre);
     int col_phase = 0;
-    auto col_load = [&](int rr, long long kk2) {  // thread 0 of the worker
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(65536) : "memory");
+    auto col_load = [&](int half, int rr, long long kk2) {  // thread 0 of the worker
+        const unsigned bs = half ? bar_s1 : bar_s0;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bs), "r"(32768) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-            "%6}], [%7];" ::"r"(buf_s),
-            "l"(&zmap), "r"(0), "r"(0), "r"(0), "r"(rr), "r"((int)kk2), "r"(bar_s)
+            "%6}], [%7];" ::"r"(half ? buf_s : pre_s),
+            "l"(&zmap), "r"(0), "r"(0), "r"(8 * half), "r"(rr), "r"((int)kk2), "r"(bs)
+            : "memory");
+    };
+    auto col_wait = [&](unsigned bs, int ph) {
+        asm volatile(
+            "{\n\t.reg .pred P;\n"
+            "CBW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+            "@!P bra CBW_%=;\n}" ::"r"(bs),
+            "r"(ph)
             : "memory");
     };
     const int bar = 1 + grp;
@@ -612,23 +630,23 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
         }
         tm_wait_st();
         if constexpr (TMA) {
-            gsync();  // the previous column's last exchange reads of buf are done
-            if (tid == 0) col_load(0, k2);
+            gsync();  // the previous column's last exchange reads of buf / pre are done
+            if (tid == 0) {
+                col_load(0, 0, k2);
+                col_load(1, 0, k2);
+            }
         }
         gsync();  // step visible
         for (int r = p.r0; r < p.r1; ++r) {
             double2 v[16];
             if constexpr (TMA) {
-                asm volatile(
-                    "{\n\t.reg .pred P;\n"
-                    "CBW_%=:\n\t"
-                    "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-                    "@!P bra CBW_%=;\n}" ::"r"(bar_s),
-                    "r"(col_phase)
-                    : "memory");
+                col_wait(bar_s0, col_phase);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = cmul(pre[tid + q * G], cmul(base, step[q]));
+                col_wait(bar_s1, col_phase);
                 col_phase ^= 1;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = cmul(buf[tid + q * G], cmul(base, step[q]));
+                for (int q = 8; q < 16; ++q) v[q] = cmul(buf[tid + (q - 8) * G], cmul(base, step[q]));
             } else {
                 const double2* col = Z + (long long)(r - p.r0) * N + k2;
 #pragma unroll
@@ -638,6 +656,9 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 }
             }
             gsync();  // previous term's last-stage reads of buf (and this term's inputs) are done
+            if constexpr (TMA) {
+                if (tid == 0 && r + 1 < p.r1) col_load(0, r + 1 - p.r0, k2);  // pre is free: a whole term ahead
+            }
             if constexpr (F2L) {
                 block_fft_2l<-1>(v, buf, tid, T, gsync);
             } else {
@@ -645,8 +666,8 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             }
             if constexpr (TMA) {
                 if (r + 1 < p.r1) {
-                    gsync();  // exchange reads done: the next term's column may land in buf
-                    if (tid == 0) col_load(r + 1 - p.r0, k2);
+                    gsync();  // exchange reads done: the next term's second half may land in buf
+                    if (tid == 0) col_load(1, r + 1 - p.r0, k2);
                 }
             }
 #pragma unroll
@@ -738,7 +759,7 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
 }
 
 // Z columns (rr*N + t1*4096 + k2, N1 = 2^log_n1 rows) as the 5-D tensor k1_passB_tm<.., TMA>
-// loads from: (re/im, t1 & 255, t1 >> 8, rr, k2), box = one column of one term
+// loads from: (re/im, t1 & 255, t1 >> 8, rr, k2), box = half a column of one term
 bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int nterms) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
@@ -752,7 +773,7 @@ bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int nt
     const cuuint64_t row = 4096ull * 16ull;  // bytes per t1 (N2 = 4096)
     cuuint64_t dims[5] = {2, 256, 16, (cuuint64_t)nterms, 4096};
     cuuint64_t strides[4] = {row, 256 * row, 4096 * row, 16};
-    cuuint32_t box[5] = {2, 256, 16, 1, 1};
+    cuuint32_t box[5] = {2, 256, 8, 1, 1};  // half a column (t1 < 2048 or >= 2048)
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Z, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -836,7 +857,7 @@ template <int L1>
 void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     if constexpr (L1 >= 2048) {
-        constexpr size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
+        size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
         PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
         CUtensorMap zmap{};
@@ -844,8 +865,10 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
             static const bool f2l = !getenv("NUFFT_PASSB_FFT3");  // A/B: three-stage FFT
             static const bool tma = !getenv("NUFFT_PASSB_NO_TMA");  // A/B: LSU column loads
             if (f2l) fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
-            if (f2l && tma && pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
+            if (f2l && tma && pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0)) {
                 fn = pl.uniform ? k1_passB_tm<L1, true, true, true> : k1_passB_tm<L1, false, true, true>;
+                SMT += sizeof(double2) * 2 * 2048;  // the two `pre` half-column buffers
+            }
         }
         set_smem(fn, SMT);
         const long long n2 = 1ll << pl.bk.log_n2;
