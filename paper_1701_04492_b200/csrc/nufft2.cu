@@ -469,6 +469,7 @@ struct Pass2Params {
     int ablate;                 // diagnostics (NUFFT_ABLATE): 1 skip sample math, 2 skip FFT math
     int deg[kRankCap];
     int deg_rel0, deg_rel1;  // relative-accuracy degrees of g_{r1-1}, g_{r1} (recurrence start)
+    int l2pf;                // fused-sample pass 2: L2 prefetch of the group's row l2pf steps ahead
 };
 #define NB_TRACE(slot)                                                                   \
     do {                                                                                 \
@@ -1573,9 +1574,15 @@ __global__ void __launch_bounds__(512, 1)
                 fs_fft_regs(v, buf, tid, T, gsync);
             }
             FS_TRACE(S0 + i, 1);
-            // this group's next row (step i + 2) is in flight during the update
+            // this group's next row (step i + 2) is in flight during the update; a later
+            // one (step i + 2 l2pf) is warmed in L2
             have = i + 2 < nt;
             if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
+            if (p.l2pf && tid == 0 && i + 2 * p.l2pf < nt) {
+                const void* nxt = Y + y_index(rr - 2 * p.l2pf, N, p.log_n2, urow, 0);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                             "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
+            }
             if (i > 0) {  // the other group's update of step i-1 is done
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
                 tm_fence_after();
@@ -1837,6 +1844,9 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     static const bool trace = getenv("NUFFT_TRACE_PASS2") != nullptr;
     static const int ablate = getenv("NUFFT_ABLATE") ? atoi(getenv("NUFFT_ABLATE")) : 0;
     p.ablate = ablate;
+    // NUFFT_FS_L2PF = k: L2 prefetch of the group's row k steps ahead (0: off)
+    static const int l2pf = getenv("NUFFT_FS_L2PF") ? atoi(getenv("NUFFT_FS_L2PF")) : 2;
+    p.l2pf = l2pf;
     unsigned long long* tr = nullptr;
     if (trace) {
         NB_CUDA(cudaMalloc(&tr, 8 * 8 * 64));
