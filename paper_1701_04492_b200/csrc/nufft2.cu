@@ -470,6 +470,7 @@ struct Pass2Params {
     int deg[kRankCap];
     int deg_rel0, deg_rel1;  // relative-accuracy degrees of g_{r1-1}, g_{r1} (recurrence start)
     int l2pf;                // fused-sample pass 2: L2 prefetch of the group's row l2pf steps ahead
+    int l2pf_pair;           // 1: only even rows prefetch (the pair's other row is in the same 128 KiB)
 };
 #define NB_TRACE(slot)                                                                   \
     do {                                                                                 \
@@ -1578,7 +1579,7 @@ __global__ void __launch_bounds__(512, 1)
             // one (step i + 2 l2pf) is warmed in L2
             have = i + 2 < nt;
             if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
-            if (p.l2pf && tid == 0 && i + 2 * p.l2pf < nt) {
+            if (p.l2pf && tid == 0 && i + 2 * p.l2pf < nt && (p.l2pf_pair == 0 || (urow & 1) == 0)) {
                 const void* nxt = Y + y_index(rr - 2 * p.l2pf, N, p.log_n2, urow, 0);
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
                              "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
@@ -1847,6 +1848,8 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     // NUFFT_FS_L2PF = k: L2 prefetch of the group's row k steps ahead (0: off)
     static const int l2pf = getenv("NUFFT_FS_L2PF") ? atoi(getenv("NUFFT_FS_L2PF")) : 2;
     p.l2pf = l2pf;
+    static const int l2pf_pair = getenv("NUFFT_FS_L2PF_PAIR") ? atoi(getenv("NUFFT_FS_L2PF_PAIR")) : 1;
+    p.l2pf_pair = l2pf_pair;
     unsigned long long* tr = nullptr;
     if (trace) {
         NB_CUDA(cudaMalloc(&tr, 8 * 8 * 64));
