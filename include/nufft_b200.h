@@ -99,6 +99,18 @@ void nufft_fft_reset_exec_counts(void);                                   /* fft
 /* number of CUDA kernels this library has launched (benchmark evidence) */
 uint64_t nufft_kernel_launch_count(void);
 
+/* ---- seeded sampler: GaussianSampler, random.hpp:14-60 (host-only) --------
+ * mt19937_64, uniform = (draw >> 11) * 2^-53, Box-Muller normals in pairs;
+ * the same seed gives the reference's x and c bit for bit.                    */
+typedef struct nufft_sampler nufft_sampler;
+int nufft_sampler_create(uint64_t seed, nufft_sampler** out);           /* GaussianSampler(seed)  :16  */
+void nufft_sampler_destroy(nufft_sampler* s);
+double nufft_sampler_normal(nufft_sampler* s);                          /* operator()             :18-34 */
+double nufft_sampler_uniform(nufft_sampler* s);                         /* uniform()              :36-38 */
+int nufft_sampler_uniform_vector(nufft_sampler* s, size_t n, double lo, double hi,
+                                 double* out);                          /* uniform_vector         :50-54 */
+int nufft_sampler_complex_vector(nufft_sampler* s, size_t n, double* out); /* complex_vector (re, im) :40-48 */
+
 /* ------------------------------------------------------------- samples */
 int nufft_normalize_samples(const double* raw, size_t n, double* out);    /* transforms.hpp:35-45 */
 int nufft_grid_assign(const double* x, size_t n, size_t grid, long* s, size_t* t,
@@ -123,6 +135,40 @@ int nufft_plan2_exec_terms(const nufft_plan2* plan, const double* c_dev, double*
                            size_t batch, size_t r_begin, size_t r_end, void* stream);
 int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, double* f,
                           size_t batch);
+
+/* ---- multi-GPU type II: the rank-K sum split across GPUs --
+ * Replaces the reference's threaded exec (exec_nufft2 with threads > 1,
+ * transforms.hpp:174-197: contiguous r-ranges per worker, partials merged):
+ * one process per GPU, an NCCL communicator between them.  Rank g evaluates
+ * terms [K g/G, K (g+1)/G) (nufft_multi_term_range), pass 2 writes its partial
+ * in bucket order in row chunks, and each chunk is summed (fp64) on the
+ * communicator's stream while the next one is computed; the receiving ranks
+ * un-permute once.  NCCL is loaded at run time (libnufft_b200.so does not link
+ * it).  Every rank passes the same c (device pointer, batch vectors of N);
+ * f receives the full transform on `root` (NUFFT_MULTI_REDUCE) or on every
+ * rank (NUFFT_MULTI_ALLREDUCE).  Ordered on `stream`.                          */
+typedef struct nufft_comm nufft_comm;
+#define NUFFT_UNIQUE_ID_BYTES 128
+enum nufft_multi_mode { NUFFT_MULTI_REDUCE = 0, NUFFT_MULTI_ALLREDUCE = 1 };
+int nufft_comm_unique_id(unsigned char* id);  /* ncclGetUniqueId; id: NUFFT_UNIQUE_ID_BYTES bytes */
+int nufft_comm_init(const unsigned char* id, int nranks, int rank, int device, nufft_comm** out);
+int nufft_comm_wrap(void* nccl_comm, int device, nufft_comm** out); /* adopt a caller-owned ncclComm_t */
+void nufft_comm_destroy(nufft_comm* comm);
+int nufft_comm_info(const nufft_comm* comm, int* nranks, int* rank, int* device);
+int nufft_multi_term_range(size_t K, int nranks, int rank, size_t* r_begin, size_t* r_end); /* host-only */
+int nufft_plan2_exec_multi(const nufft_plan2* plan, const double* c_dev, double* f_dev, size_t batch,
+                           nufft_comm* comm, int root, int mode, void* stream);
+/* The pieces exec_multi is built from, for callers that bring their own
+ * collective (e.g. torch.distributed): the partial over terms [r_begin, r_end)
+ * of one vector in bucket order, the bucket-order ranges of the row chunks
+ * exec_multi reduces one at a time (offsets[0..nchunks]), and the final
+ * bucket-order -> natural-order permutation f[perm[i]] = fs[i].  Fused plans
+ * (power-of-two N >= 256) only.                                               */
+int nufft_plan2_exec_terms_sorted(const nufft_plan2* plan, const double* c_dev, double* fs_dev,
+                                  size_t r_begin, size_t r_end, void* stream);
+int nufft_plan2_reduce_chunks(const nufft_plan2* plan, int nchunks, size_t* offsets);
+int nufft_plan2_unpermute(const nufft_plan2* plan, const double* fs_dev, double* f_dev, size_t batch,
+                          void* stream);
 /* exec (batch 1, fused path) recording CUDA events before pass 1, between the passes
  * and after pass 2 on `stream` into timing slot `slot` (no synchronization);
  * timing_read sums the per-pass device times of slots [0, nslots).  Used by

@@ -102,6 +102,22 @@ _SIGS = {
     "nufft_plan2d2_exec": (_i, [_vp, _vp, _vp, _sz, _vp]),
     "nufft_plan2d2_exec_host": (_i, [_vp, _vp, _sz, _sz, _vp, _sz]),
     "nufft_plan2d2_exec_host_impl": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _i]),
+    "nufft_comm_unique_id": (_i, [_vp]),
+    "nufft_comm_init": (_i, [_vp, _i, _i, _i, C.POINTER(_vp)]),
+    "nufft_comm_wrap": (_i, [_vp, _i, C.POINTER(_vp)]),
+    "nufft_comm_destroy": (None, [_vp]),
+    "nufft_comm_info": (_i, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "nufft_multi_term_range": (_i, [_sz, _i, _i, C.POINTER(_sz), C.POINTER(_sz)]),
+    "nufft_plan2_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
+    "nufft_plan2_exec_terms_sorted": (_i, [_vp, _vp, _vp, _sz, _sz, _vp]),
+    "nufft_plan2_reduce_chunks": (_i, [_vp, _i, _vp]),
+    "nufft_plan2_unpermute": (_i, [_vp, _vp, _vp, _sz, _vp]),
+    "nufft_sampler_create": (_i, [C.c_uint64, C.POINTER(_vp)]),
+    "nufft_sampler_destroy": (None, [_vp]),
+    "nufft_sampler_normal": (C.c_double, [_vp]),
+    "nufft_sampler_uniform": (C.c_double, [_vp]),
+    "nufft_sampler_uniform_vector": (_i, [_vp, _sz, C.c_double, C.c_double, _vp]),
+    "nufft_sampler_complex_vector": (_i, [_vp, _sz, _vp]),
 }
 
 

@@ -26,6 +26,7 @@ __all__ = [
     "device_count", "ToeplitzOperator", "toeplitz_from_first_column", "toeplitz_from_normal",
     "toeplitz_from_gram", "toeplitz_matvec", "cg_solve_toeplitz", "inufft2", "inufft1",
     "default_cg_max_iter", "exec_nufft1_adjoint", "inufft2_device", "nudft_direct", "nudft2d_direct",
+    "GaussianSampler",
 ]
 
 
@@ -281,6 +282,29 @@ class Plan2(_PlanBase):
         """exec through the host-pointer C-ABI call (copies inside)."""
         _check(lib().nufft_plan2_exec_host(self._h, c_ptr, self.size(), f_ptr, batch))
 
+    # ---- multi-GPU (nufft_plan2_exec_multi and its pieces; parallel.py)
+    def execute_multi_device(self, c_ptr: int, f_ptr: int, comm, batch: int = 1, stream: int = 0,
+                             root: int = 0, allreduce: bool = False) -> None:
+        """Rank-split exec over an NCCL communicator (parallel.NcclComm): this rank's
+        terms, chunked reduce, f complete on `root` (or on every rank)."""
+        _check(lib().nufft_plan2_exec_multi(self._h, c_ptr, f_ptr, batch, comm.handle, root,
+                                            1 if allreduce else 0, stream or None))
+
+    def execute_terms_sorted_device(self, c_ptr: int, fs_ptr: int, r_begin: int, r_end: int,
+                                    stream: int = 0) -> None:
+        """Partial sum over terms [r_begin, r_end) in bucket (plan) order."""
+        _check(lib().nufft_plan2_exec_terms_sorted(self._h, c_ptr, fs_ptr, r_begin, r_end, stream or None))
+
+    def reduce_chunks(self, nchunks: int) -> np.ndarray:
+        """Bucket-order offsets [0 .. N] of the row chunks exec_multi reduces one at a time."""
+        off = np.zeros(nchunks + 1, np.uint64)
+        _check(lib().nufft_plan2_reduce_chunks(self._h, nchunks, _ptr(off)))
+        return off.astype(np.int64)
+
+    def unpermute_device(self, fs_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
+        """f[perm[i]] = fs[i] (bucket order -> sample order)."""
+        _check(lib().nufft_plan2_unpermute(self._h, fs_ptr, f_ptr, batch, stream or None))
+
     def adjoint(self, f) -> np.ndarray:
         f = _c128(f)
         out = np.empty_like(f)
@@ -382,6 +406,38 @@ class Plan2D(_PlanBase):
 
     def execute_device(self, C_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
         _check(lib().nufft_plan2d2_exec(self._h, C_ptr, f_ptr, batch, stream or None))
+
+
+class GaussianSampler:
+    """The reference's seeded sampler (random.hpp:14-60; drop-in include/nufft/random.hpp):
+    mt19937_64, 53-bit uniforms, Box-Muller normals in pairs.  Host-only."""
+
+    def __init__(self, seed: int):
+        h = C.c_void_p()
+        _check(lib().nufft_sampler_create(seed, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            lib().nufft_sampler_destroy(self._h)
+        except Exception:
+            pass
+
+    def __call__(self) -> float:
+        return lib().nufft_sampler_normal(self._h)
+
+    def uniform(self) -> float:
+        return lib().nufft_sampler_uniform(self._h)
+
+    def uniform_vector(self, n: int, lo: float, hi: float) -> np.ndarray:
+        out = np.empty(n)
+        _check(lib().nufft_sampler_uniform_vector(self._h, n, lo, hi, _ptr(out)))
+        return out
+
+    def complex_vector(self, n: int) -> np.ndarray:
+        out = np.empty(n, np.complex128)
+        _check(lib().nufft_sampler_complex_vector(self._h, n, _ptr(out)))
+        return out
 
 
 def plan_nufft2(x_raw, epsilon: float, device: int = -1) -> Plan2:

@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I" + os.path.join(HERE, "..", "include")]
-# NB_NVCC_EXTRA: extra nvcc flags for experiment builds (e.g. "-DNB_FS_TRACE")
+# NB_NVCC_EXTRA: extra nvcc flags for experiment builds (e.g. "-Xptxas=-warn-spills")
 FLAGS += os.environ.get("NB_NVCC_EXTRA", "").split()
 
 
@@ -71,20 +71,26 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     return LIB
 
 
-EXAMPLE_SRC = os.path.join(HERE, "..", "tests", "cpp", "example_dropin.cpp")
+CPP_DIR = os.path.join(HERE, "..", "tests", "cpp")
+# C++ programs written against the drop-in headers (include/nufft) and linked with
+# the library: the usage example / self-check, and the end-to-end timing of
+# exec_nufft2(plan, std::vector) that bench.py reports as e2e.dropin_pageable
+CPP_PROGRAMS = ("example_dropin", "bench_dropin")
 EXAMPLE_BIN = os.path.join(OBJ, "example_dropin")
+BENCH_DROPIN_BIN = os.path.join(OBJ, "bench_dropin")
 
 
 def _build_example() -> None:
-    """The C++ drop-in usage example (include/nufft headers + libnufft_b200.so)."""
-    if os.path.exists(EXAMPLE_BIN) and os.path.getmtime(EXAMPLE_BIN) >= max(
-            os.path.getmtime(LIB), os.path.getmtime(EXAMPLE_SRC)):
-        return
-    r = subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(HERE, "..", "include"),
-                        EXAMPLE_SRC, "-o", EXAMPLE_BIN, "-L" + HERE, "-lnufft_b200",
-                        "-Wl,-rpath,$ORIGIN/.."], capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("example build failed:\n" + r.stderr)
+    for name in CPP_PROGRAMS:
+        src = os.path.join(CPP_DIR, name + ".cpp")
+        exe = os.path.join(OBJ, name)
+        if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(LIB), os.path.getmtime(src)):
+            continue
+        r = subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(HERE, "..", "include"),
+                            src, "-o", exe, "-L" + HERE, "-lnufft_b200",
+                            "-Wl,-rpath,$ORIGIN/.."], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"{name} build failed:\n" + r.stderr)
 
 
 if __name__ == "__main__":

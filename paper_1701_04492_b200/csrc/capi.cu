@@ -15,52 +15,16 @@
 #include <vector>
 
 #include "../../include/nufft_b200.h"
+#include "handles.hpp"
 #include "lowrank_host.hpp"
 #include "plans.hpp"
 
-struct nufft_plan2 {
-    nb::CorePlan core;
-    // per-pass timing events for the benchmark (exec_timed / timing_read)
-    mutable std::mutex timing_mu;
-    mutable std::vector<std::array<cudaEvent_t, 3>> timing;
-    ~nufft_plan2() {
-        for (auto& e : timing)
-            for (auto& x : e) cudaEventDestroy(x);
-    }
-};
-struct nufft_plan1 {
-    nb::CorePlan core;
-};
-struct nufft_plan3 {
-    nb::Plan3State st;
-};
-struct nufft_plan2d {
-    nb::Plan2DState st;
-};
-struct nufft_toeplitz {
-    nb::ToeplitzState st;
-};
-
 namespace {
 
-thread_local std::string g_err;
+using nb::guard;
+using nb::DeviceRestore;
 
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return NUFFT_OK;
-    } catch (const nb::Error& e) {
-        g_err = e.what();
-        return e.code;
-    } catch (const std::bad_alloc& e) {
-        g_err = std::string("host allocation failed: ") + e.what();
-        return NUFFT_OUT_OF_MEMORY;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return NUFFT_INTERNAL;
-    }
-}
+constexpr int kMaxTimingSlots = 1 << 16;  // exec_timed event slots per plan
 
 cudaStream_t as_stream(void* s) { return s ? static_cast<cudaStream_t>(s) : cudaStreamPerThread; }
 
@@ -180,9 +144,16 @@ void cols_fft(double2* d, size_t rows, size_t cols, cudaStream_t s, int dev) {
 
 }  // namespace
 
+namespace nb {
+std::string& last_error() {
+    thread_local std::string msg;
+    return msg;
+}
+}  // namespace nb
+
 extern "C" {
 
-const char* nufft_last_error(void) { return g_err.c_str(); }
+const char* nufft_last_error(void) { return nb::last_error().c_str(); }
 int nufft_abi_version(void) { return NUFFT_B200_ABI_VERSION; }
 int nufft_device_count(int* count) {
     return guard([&] {
@@ -382,7 +353,7 @@ static int plan2_create_impl(const double* x, bool on_dev, size_t n, double eps,
         cudaStream_t s = cudaStreamPerThread;
         nb::assign_samples(c.ax, x, on_dev, n, n, s);
         nb::finish_core(c, c.ax.gamma, s);
-        if (!c.fused || getenv("NUFFT_PLAN_BINS")) nb::build_bins(c, s);
+        if (!c.fused) nb::build_bins(c, s);
         NB_CUDA(cudaStreamSynchronize(s));
         *out = p.release();
     });
@@ -396,9 +367,12 @@ int nufft_plan2_create_device(const double* x_raw_dev, size_t n, double epsilon,
 }
 void nufft_plan2_destroy(nufft_plan2* plan) {
     if (!plan) return;
-    cudaSetDevice(plan->core.device);
+    DeviceRestore restore;
+    const int dev = plan->core.device;
+    cudaSetDevice(dev);
     cudaDeviceSynchronize();
     delete plan;
+    nb::trim_scratch(dev);
 }
 int nufft_plan2_info(const nufft_plan2* plan, nufft_plan_info* info) {
     return guard([&] { fill_info(plan->core, info); });
@@ -441,6 +415,7 @@ int nufft_plan2_exec_timed(const nufft_plan2* plan, const double* c_dev, double*
         const nb::CorePlan& p = plan->core;
         NB_CUDA(cudaSetDevice(p.device));
         if (!p.fused) nb::throw_invalid("exec_timed: plan does not use the fused two-pass path");
+        if (slot < 0 || slot >= kMaxTimingSlots) nb::throw_invalid("exec_timed: slot out of range");
         cudaEvent_t* ev = nullptr;
         {
             std::lock_guard<std::mutex> lock(plan->timing_mu);
@@ -460,7 +435,7 @@ int nufft_plan2_timing_read(const nufft_plan2* plan, int nslots, double* ms_pass
                             double* ms_pass2) {
     return guard([&] {
         std::lock_guard<std::mutex> lock(plan->timing_mu);
-        if (nslots > (int)plan->timing.size()) nb::throw_invalid("timing_read: slot out of range");
+        if (nslots < 0 || nslots > (int)plan->timing.size()) nb::throw_invalid("timing_read: slot out of range");
         double a = 0, b = 0;
         for (int i = 0; i < nslots; ++i) {
             auto& e = plan->timing[i];
@@ -483,20 +458,45 @@ int nufft_plan2_exec(const nufft_plan2* plan, const double* c_dev, double* f_dev
 // host->device copy of c_{b+1} and the device->host copy of f_{b-1} overlap the
 // transform of vector b (the PCIe copies of one 2^24 vector take longer than its
 // transform).  Results are identical to the one-shot path (same kernels per vector).
+// The overlap needs page-locked host buffers: with pageable memory the driver
+// stages every copy and the D2H blocks the host, so the batch then runs
+// copy / transform / copy in sequence (same results).
+namespace {
+struct PipeStreams {  // streams + events, drained before anything they touch is freed
+    cudaStream_t st[3] = {};
+    cudaEvent_t ev[3][2] = {};
+    cudaEvent_t ready = nullptr;
+    PipeStreams() {
+        for (auto& x : st) NB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (auto& e : ev)
+            for (auto& x : e) NB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        NB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    }
+    ~PipeStreams() {
+        for (auto& x : st)
+            if (x) cudaStreamSynchronize(x);
+        for (auto& e : ev)
+            for (auto& x : e)
+                if (x) cudaEventDestroy(x);
+        if (ready) cudaEventDestroy(ready);
+        for (auto& x : st)
+            if (x) cudaStreamDestroy(x);
+    }
+};
+}  // namespace
+
 static void plan2_host_pipelined(const nb::CorePlan& p, const double* c, double* f, size_t batch) {
     const size_t nd = 2 * p.n;  // doubles per vector
     cudaStream_t s0 = cudaStreamPerThread;
-    cudaStream_t st[3];
-    cudaEvent_t ev[3][2];
-    for (auto& x : st) NB_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-    for (auto& e : ev)
-        for (auto& x : e) NB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    // declared before the streams: on any exit the streams are drained first,
+    // then the slots go back to the pool (stream-ordered on s0)
+    nb::DevBuf din(8 * nd * 2, s0), dout(8 * nd * 2, s0);
     {
-        nb::DevBuf din(8 * nd * 2, s0), dout(8 * nd * 2, s0);
-        cudaEvent_t ready;
-        NB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        NB_CUDA(cudaEventRecord(ready, s0));
-        for (auto& x : st) NB_CUDA(cudaStreamWaitEvent(x, ready, 0));
+        PipeStreams ps;
+        auto& st = ps.st;
+        auto& ev = ps.ev;
+        NB_CUDA(cudaEventRecord(ps.ready, s0));
+        for (auto& x : st) NB_CUDA(cudaStreamWaitEvent(x, ps.ready, 0));
         enum { H2D = 0, COMP = 1, D2H = 2 };
         for (size_t b = 0; b < batch; ++b) {
             const int slot = (int)(b & 1);
@@ -515,12 +515,7 @@ static void plan2_host_pipelined(const nb::CorePlan& p, const double* c, double*
             NB_CUDA(cudaEventRecord(ev[D2H][slot], st[D2H]));
         }
         for (auto& x : st) NB_CUDA(cudaStreamSynchronize(x));
-        NB_CUDA(cudaEventDestroy(ready));
     }
-    NB_CUDA(cudaStreamSynchronize(s0));
-    for (auto& e : ev)
-        for (auto& x : e) NB_CUDA(cudaEventDestroy(x));
-    for (auto& x : st) NB_CUDA(cudaStreamDestroy(x));
     nb::fft_count(p.n, p.K * batch);
 }
 int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, double* f,
@@ -588,9 +583,12 @@ int nufft_plan1_create(const double* omega, size_t n, double epsilon, int device
 }
 void nufft_plan1_destroy(nufft_plan1* plan) {
     if (!plan) return;
-    cudaSetDevice(plan->core.device);
+    DeviceRestore restore;
+    const int dev = plan->core.device;
+    cudaSetDevice(dev);
     cudaDeviceSynchronize();
     delete plan;
+    nb::trim_scratch(dev);
 }
 int nufft_plan1_info(const nufft_plan1* plan, nufft_plan_info* info) {
     return guard([&] { fill_info(plan->core, info); });
@@ -705,9 +703,12 @@ int nufft_toeplitz_from_gram(const nufft_plan1* plan, nufft_toeplitz** out) {
 }
 void nufft_toeplitz_destroy(nufft_toeplitz* op) {
     if (!op) return;
-    cudaSetDevice(op->st.device);
+    DeviceRestore restore;
+    const int dev = op->st.device;
+    cudaSetDevice(dev);
     cudaDeviceSynchronize();
     delete op;
+    nb::trim_scratch(dev);
 }
 int nufft_toeplitz_size(const nufft_toeplitz* op, size_t* n) {
     return guard([&] { *n = op->st.n; });
@@ -783,7 +784,7 @@ static nb::CgResult inufft2_dev(const nufft_plan2* plan, const nufft_toeplitz* o
     std::unique_ptr<nufft_toeplitz> own;
     if (!op) {
         nufft_toeplitz* raw = nullptr;
-        if (nufft_toeplitz_from_normal(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, g_err);
+        if (nufft_toeplitz_from_normal(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, nb::last_error());
         own.reset(raw);
         op = raw;
     }
@@ -826,7 +827,7 @@ int nufft_inufft1_host(const nufft_plan1* plan, const nufft_toeplitz* op, const 
         std::unique_ptr<nufft_toeplitz> own;
         if (!op) {
             nufft_toeplitz* raw = nullptr;
-            if (nufft_toeplitz_from_gram(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, g_err);
+            if (nufft_toeplitz_from_gram(plan, &raw) != NUFFT_OK) throw nb::Error(nb::kInternal, nb::last_error());
             own.reset(raw);
             op = raw;
         }
@@ -931,9 +932,12 @@ int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, siz
 }
 void nufft_plan3_destroy(nufft_plan3* plan) {
     if (!plan) return;
-    cudaSetDevice(plan->st.a.device);
+    DeviceRestore restore;
+    const int dev = plan->st.a.device;
+    cudaSetDevice(dev);
     cudaDeviceSynchronize();
     delete plan;
+    nb::trim_scratch(dev);
 }
 int nufft_plan3_info(const nufft_plan3* plan, nufft_plan_info* info) {
     return guard([&] {
@@ -1013,9 +1017,12 @@ int nufft_plan2d2_create(const double* x_raw, const double* y_raw, size_t count_
 }
 void nufft_plan2d2_destroy(nufft_plan2d* plan) {
     if (!plan) return;
-    cudaSetDevice(plan->st.device);
+    DeviceRestore restore;
+    const int dev = plan->st.device;
+    cudaSetDevice(dev);
     cudaDeviceSynchronize();
     delete plan;
+    nb::trim_scratch(dev);
 }
 int nufft_plan2d2_info(const nufft_plan2d* plan, nufft_plan_info* info) {
     return guard([&] {

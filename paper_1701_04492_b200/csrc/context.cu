@@ -23,11 +23,30 @@ std::atomic<unsigned long long> g_launches{0};
 std::map<size_t, uint64_t> g_counts;
 }  // namespace
 
-void setup_mempool(int device) {
-    cudaMemPool_t pool;
-    NB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+namespace {
+cudaMemPool_t create_pool(int device) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    NB_CUDA(cudaMemPoolCreate(&pool, &props));
     uint64_t threshold = UINT64_MAX;
     NB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    return pool;
+}
+}  // namespace
+
+void trim_scratch(int device) {
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_ctx_mu);
+        auto it = g_ctx.find(device);
+        if (it == g_ctx.end()) return;
+        pool = it->second->pool;
+    }
+    cudaMemPoolTrimTo(pool, 0);  // unused blocks only; live allocations are untouched
 }
 
 DeviceCtx& DeviceCtx::get(int device) {
@@ -38,7 +57,7 @@ DeviceCtx& DeviceCtx::get(int device) {
     ctx->device = device;
     NB_CUDA(cudaSetDevice(device));
     ctx->sms = sm_count(device);
-    setup_mempool(device);
+    ctx->pool = create_pool(device);
     for (int l = 1; l <= 12; ++l) {
         const int L = 1 << l;
         double2* p = nullptr;
@@ -57,7 +76,9 @@ void DevBuf::alloc(size_t bytes, cudaStream_t s) {
     release();
     s_ = s;
     if (bytes == 0) bytes = 16;
-    NB_CUDA(cudaMallocAsync(&p_, bytes, s));
+    int dev = 0;
+    NB_CUDA(cudaGetDevice(&dev));
+    NB_CUDA(cudaMallocFromPoolAsync(&p_, bytes, DeviceCtx::get(dev).pool, s));
 }
 void DevBuf::release() {
     if (p_) cudaFreeAsync(p_, s_);

@@ -20,13 +20,17 @@ struct DeviceCtx {
     int device = 0;
     int sms = 0;
     const double2* tw[13] = {};
+    cudaMemPool_t pool = nullptr;  // the library's own scratch pool (never the device default)
     static DeviceCtx& get(int device);
     const double2* table(int L) const { return tw[ilog2(static_cast<size_t>(L))]; }
 };
 
-// RAII stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync on the
-// device's default memory pool, whose release threshold is raised so that
-// repeated executions reuse memory instead of re-allocating).
+// RAII stream-ordered device buffer (cudaMallocFromPoolAsync / cudaFreeAsync on
+// the library's private memory pool of the current device: its release
+// threshold is raised so repeated executions reuse scratch instead of
+// re-allocating, and trim_scratch() hands the cached memory back — the
+// device's default pool, which PyTorch and other libraries share, is left
+// alone).
 class DevBuf {
   public:
     DevBuf() = default;
@@ -66,7 +70,8 @@ class DevArray {
     size_t bytes_ = 0;
 };
 
-void setup_mempool(int device);
+// release the scratch cached in the device's private pool (plan destruction)
+void trim_scratch(int device);
 
 // ---- logical FFT execution counters (fft.hpp:91-95,126-137 test hook) -----
 void fft_count(size_t n, uint64_t times = 1);

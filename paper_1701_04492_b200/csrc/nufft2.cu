@@ -28,8 +28,6 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
-#include <cstdio>
-#include <cstdlib>
 
 #include "bessel.cuh"
 #include "fft_block.cuh"
@@ -465,17 +463,10 @@ struct Pass2Params {
     const unsigned* skey;
     const int* perm;
     const int* rowoff;
-    unsigned long long* trace;  // diagnostics: per-iteration clock64 stamps of CTA 0 (nullptr = off)
-    int ablate;                 // diagnostics (NUFFT_ABLATE): 1 skip sample math, 2 skip FFT math
+    long long row0, row1;  // rows [row0, row1) of this launch (multi-GPU chunked pass 2)
     int deg[kRankCap];
     int deg_rel0, deg_rel1;  // relative-accuracy degrees of g_{r1-1}, g_{r1} (recurrence start)
-    int l2pf;                // fused-sample pass 2: L2 prefetch of the group's row l2pf steps ahead
-    int l2pf_pair;           // 1: only even rows prefetch (the pair's other row is in the same 128 KiB)
 };
-#define NB_TRACE(slot)                                                                   \
-    do {                                                                                 \
-        if (p.trace && blockIdx.x == 0 && tid == 0) p.trace[(slot)] = clock64();           \
-    } while (0)
 
 // One Horner step in r for the thread's samples: acc <- acc*(i h) + g_r(h^2) X_r[t2].
 // Samples go in chunks of C with a straight-line series per chunk; slots past
@@ -512,6 +503,13 @@ __device__ __forceinline__ void horner_step(double2 (&acc)[Q], int r, int deg, c
 // as the reference does (transforms.hpp:60-64,84-86), or — for type-I cores,
 // whose delta = omega - round(omega) is not recoverable from omega/N
 // (transforms.hpp:262-272) — read from the plan's sorted copies.
+// where sample idx (bucket order) of this launch writes: f[perm[idx]], or the
+// bucket-order partial fs[idx] when perm is null (multi-GPU r-split: the partials
+// are reduced in bucket order and un-permuted once, nufft2_multi.cu)
+__device__ __forceinline__ long long out_index(const Pass2Params& p, int idx) {
+    return p.perm ? (long long)p.perm[idx] : (long long)idx;
+}
+
 __device__ __forceinline__ void sample_geom(const Pass2Params& p, int idx, int& t2, double& h) {
     if (p.ds) {
         h = half_phase(p.ds[idx]);
@@ -531,7 +529,6 @@ __device__ __forceinline__ void sample_geom(const Pass2Params& p, int idx, int& 
 template <int Q, int G>
 __device__ __forceinline__ void load_samples(const Pass2Params& p, int cb, int cnt, int tid,
                                              int* st2, double* sh, double2 (&acc)[Q]) {
-    const double dn = (double)p.n;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         acc[q] = make_double2(0.0, 0.0);
@@ -575,7 +572,7 @@ __device__ __forceinline__ void store_samples(const Pass2Params& p, int cb, int 
                 sincos(2.0 * h, &sn, &cs);
                 out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
             }
-            __stcs(f + p.perm[cb + i], out);
+            __stcs(f + out_index(p, cb + i), out);
         }
     }
 }
@@ -599,9 +596,8 @@ __global__ void __launch_bounds__(L2 / 16)
     twiddle_init<L2>(T, t16, tid);
     __syncthreads();
     const long long N = p.n;
-    const long long n1 = 1ll << p.log_n1;
     double2* xb = block_fft_free_buf<L2>(buf0, buf1);
-    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+    for (long long row = p.row0 + blockIdx.x; row < p.row1; row += gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         for (int cb = beg; cb < end; cb += CAP) {
             const int cnt = min(CAP, end - cb);
@@ -635,66 +631,36 @@ __global__ void __launch_bounds__(L2 / 16)
     }
 }
 
-// mbarrier helpers (shared::cta)
-__device__ __forceinline__ void mbar_init(unsigned long long* m, int count) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, int parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
-    asm volatile(
-        "{\n\t.reg .pred P;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra WAIT_%=;\n}" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-// async arrive when this thread's prior cp.async operations have completed
-__device__ __forceinline__ void mbar_cp_async_arrive(unsigned long long* m) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(m);
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gsrc) : "memory");
-}
-
-// Warp-specialized rows (L2 >= 1024): threads [0, G) run the row FFTs, threads
-// [G, 2G) own the samples.  X_r alternates between two shared buffers.
-//   FULL_b (named barrier): X_r is in buffer b -> sample warps may gather.
-//   staged_b (mbarrier):    sample warps finished with buffer b and the
-//                           Y row of term r-2 has landed in it (cp.async
-//                           issued by the sample warps, completion tracked
-//                           asynchronously) -> FFT warps may start FFT(r-2).
-// The sample warps' Horner updates of step r and the staging copy overlap
-// the FFT of r-1; no warp blocks on a global load except the first two rows
-// of a chunk.
+// Warp-specialized rows (L2 = 1024, e.g. N = 2^20): threads [0, G) run the
+// row FFTs, threads [G, G + S) own the samples.  X_r alternates between two
+// shared buffers:
+//   FULL_b  (named barrier): X_r is in buffer b -> sample warps may gather;
+//   EMPTY_b (named barrier): the gathers from b are done -> FFT of step i + 2.
+// The sample warps' Horner updates of step r overlap the FFT of r-1.
 // Sample role width: S = 1.5 G threads holding QS = 12 samples each
 // (capacity 18 G = 1.125 N2, above the Poisson spread of an iid row): more
 // warps than the FFT role, because the per-term sample update is a chain of
 // dependent shared loads and FMAs that needs many warps in flight.
-template <int L2, int X2>
+template <int L2>
 struct WsShape {
-    static constexpr int G = L2 / 16;   // FFT role threads
-    static constexpr int S = G * X2 / 2;  // sample role threads (X2 = 2: as many as the FFT role)
-    static constexpr int QS = (18 * G + S - 1) / S;          // samples per sample thread
-    static constexpr int CAP = QS * S;  // samples per chunk
+    static constexpr int G = L2 / 16;                // FFT role threads
+    static constexpr int S = G * 3 / 2;              // sample role threads
+    static constexpr int QS = (18 * G + S - 1) / S;  // samples per sample thread
+    static constexpr int CAP = QS * S;               // samples per chunk
     static constexpr int ALL = G + S;
 };
 
-template <int L2, bool UNIFORM, int X2, bool STAGE>
-__global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
+template <int L2, bool UNIFORM>
+__global__ void __launch_bounds__(WsShape<L2>::ALL, 1)
     k2_pass2_ws(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
-    using W = WsShape<L2, X2>;
+    using W = WsShape<L2>;
     constexpr int G = W::G;
     constexpr int S = W::S;
     constexpr int Q = W::QS;
     constexpr int CAP = W::CAP;
     constexpr int ALL = W::ALL;
-    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_FFT = 5, BAR_SMP = 6;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_FFT = 5;
     extern __shared__ double2 smem[];
-    __shared__ unsigned long long staged[2];
     double2* bufs = smem;  // 2 x padded_len(L2)
     double2* t16 = bufs + 2 * padded_len(L2);
     double* sh = reinterpret_cast<double*>(t16 + FftShapeX<L2>::TW_LEN);
@@ -704,17 +670,10 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
     twiddle_table_build<L2>(t16, threadIdx.x, ALL);
     Twiddles<L2> T;
     if (fft_warp) twiddle_init<L2>(T, t16, tid);
-    if (threadIdx.x == 0) {
-        mbar_init(&staged[0], S);
-        mbar_init(&staged[1], S);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     __syncthreads();
-    int phase[2] = {0, 0};  // completed stagings per buffer (identical in both roles)
     const long long N = p.n;
-    const long long n1 = 1ll << p.log_n1;
     const long long n2 = 1ll << p.log_n2;
-    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+    for (long long row = p.row0 + blockIdx.x; row < p.row1; row += gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         for (int cb = beg; cb < end; cb += CAP) {
             const int cnt = min(CAP, end - cb);
@@ -725,38 +684,23 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
                     const int b = i & 1;
                     double2* buf = bufs + b * padded_len(L2);
                     const int rr = r - p.r0;
-                    if (tid == 0 && rr >= 2 && (row & 1) == 0) {  // warm L2 for the staging copy
+                    if (tid == 0 && rr >= 2 && (row & 1) == 0) {  // warm L2 with a later row pair
                         const void* nxt = Y + y_index(rr - 2, N, p.log_n2, row, 0);
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
                                      "r"((unsigned)(2 * n2 * sizeof(double2))) : "memory");
                     }
                     double2 v[16];
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 0);
-                    if (!STAGE) {
-                        const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
+                    const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
-                        if (i >= 2) nbar_sync(BAR_EMPTY + b, ALL);  // samples done with X_{r+2}
-                    } else if (i >= 2) {
-                        mbar_wait(&staged[b], phase[b] & 1);
-                        ++phase[b];
-                        load_stage_input<L2>(v, buf, tid);
-                        nbar_sync(BAR_FFT, G);  // all inputs read before stage 1 reuses buf
-                    } else {
-                        const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
-                    }
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 1);
+                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    if (i >= 2) nbar_sync(BAR_EMPTY + b, ALL);  // samples done with X_{r+2}
                     block_fft_1buf<L2, -1>(v, buf, tid, T, [] { nbar_sync(BAR_FFT, G); });
                     nbar_sync(BAR_FFT, G);  // last-stage reads of buf done
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 2);
                     nbar_arrive(BAR_FULL + b, ALL);
                 }
-                if (!STAGE)
-                    for (int i = max(0, nt - 2); i < nt; ++i) nbar_sync(BAR_EMPTY + (i & 1), ALL);
+                for (int i = max(0, nt - 2); i < nt; ++i) nbar_sync(BAR_EMPTY + (i & 1), ALL);
             } else {
                 double2 acc[Q];
                 load_samples<Q, S>(p, cb, cnt, tid, st2, sh, acc);
@@ -765,7 +709,6 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
                     const int b = i & 1;
                     double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, ALL);
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 4);
                     if constexpr (UNIFORM) {
 #pragma unroll
                         for (int q = 0; q < Q; ++q) {
@@ -775,233 +718,12 @@ __global__ void __launch_bounds__(WsShape<L2, X2>::ALL, 1)
                     } else {
                         horner_step<Q, S>(acc, r, p.deg[r], xb, st2, sh, tid);
                     }
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 5);
-                    if (!STAGE) {
-                        nbar_arrive(BAR_EMPTY + b, ALL);
-                    } else if (i + 2 < nt) {  // stage the Y row of term r-2 into this buffer
-                        nbar_sync(BAR_SMP, S);  // every sample warp is done reading X_r here
-                        const double2* src = Y + y_index(r - 2 - p.r0, N, p.log_n2, row, 0);
-#pragma unroll
-                        for (int q = 0; q < L2 / S; ++q) {
-                            const int k2 = tid + q * S;
-                            cp_async16(xb + pad16(k2), src + 2 * k2);
-                        }
-                        mbar_cp_async_arrive(&staged[b]);
-                        ++phase[b];
-                    }
-                    if (row == blockIdx.x && cb == beg) NB_TRACE(8 * i + 6);
+                    nbar_arrive(BAR_EMPTY + b, ALL);
                 }
                 store_samples<Q, S, UNIFORM>(p, cb, cnt, tid, sh, acc, f);
             }
             __syncthreads();  // st2 / sh / buffers free for the next chunk
         }
-    }
-}
-
-// ---------------------------------------------------------------- TMEM variant
-// The sample role keeps its per-sample metadata in tensor memory (tmem.cuh:
-// h: 2 columns, t2: 1 column per sample), which frees the shared memory for
-// a third row buffer.
-// Triple-buffered, warp-specialized rows (L2 >= 1024):
-//   buffer b = i % 3 carries, in turn, the staged Y row of step i (cp.async by
-//   the sample warps one full step ahead), the FFT exchange of step i, and
-//   X_r of step i for the sample gathers.  Ordering: staged[b] (mbarrier,
-//   sample cp.async arrivals) -> FFT warps; FULL_b (named barrier) -> sample
-//   warps; the sample warps re-stage b only after all of them have gathered.
-//   No warp waits on a global load inside the term loop.
-template <int L2>
-struct TmShape {
-    static constexpr int G = L2 / 16;
-    static constexpr int S = 3 * G / 2;
-    static constexpr int Q = 12;  // samples per sample thread (3 chunks of 4)
-    static constexpr int CAP = Q * S;
-    static constexpr int ALL = G + S;
-    static constexpr int COLS_PER_THREAD = 3 * Q;                  // h (2 each) + t2 (1 each)
-    static constexpr int BLOCKS = (ALL / 32 + 3) / 4;              // column blocks per lane
-    static constexpr int TM_COLS = (BLOCKS * COLS_PER_THREAD <= 256) ? 256 : 512;
-    static constexpr size_t SMEM = sizeof(double2) * (3 * padded_len(L2) + FftShapeX<L2>::TW_LEN);
-    static_assert(BLOCKS * COLS_PER_THREAD <= 512, "TMEM columns");
-    static_assert(SMEM <= 227 * 1024, "pass 2 (TMEM variant) shared memory");
-    static_assert(CAP >= 18 * G, "sample capacity");
-};
-
-template <int L2, bool UNIFORM>
-__global__ void __launch_bounds__(TmShape<L2>::ALL, 1)
-    k2_pass2_tm(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
-    using W = TmShape<L2>;
-    constexpr int G = W::G;
-    constexpr int S = W::S;
-    constexpr int Q = W::Q;
-    constexpr int CAP = W::CAP;
-    constexpr int ALL = W::ALL;
-    constexpr int BAR_FULL = 1, BAR_FFT = 5, BAR_SMP = 6;  // FULL_b = 1..3
-    extern __shared__ double2 smem[];
-    __shared__ unsigned long long staged[3];
-    __shared__ unsigned tmem_base;
-    double2* bufs = smem;  // 3 x padded_len(L2)
-    double2* t16 = bufs + 3 * padded_len(L2);
-    const bool fft_warp = threadIdx.x < G;
-    const int tid = fft_warp ? threadIdx.x : threadIdx.x - G;
-    const int warp = threadIdx.x >> 5;
-    twiddle_table_build<L2>(t16, threadIdx.x, ALL);
-    Twiddles<L2> T;
-    if (fft_warp) twiddle_init<L2>(T, t16, tid);
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < 3; ++b) mbar_init(&staged[b], S);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == G / 32) {  // first sample warp owns the TMEM allocation
-        const unsigned a = (unsigned)__cvta_generic_to_shared(&tmem_base);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a),
-                     "r"((unsigned)W::TM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this thread's columns: block warp/4 of its lane, 3Q columns: [h lo,hi x Q][t2 x Q]
-    const unsigned tcol = tm_lane_base(tmem_base) + (unsigned)((warp >> 2) * W::COLS_PER_THREAD);
-    int phase[3] = {0, 0, 0};
-    const long long N = p.n;
-    const long long n1 = 1ll << p.log_n1;
-    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
-        const int beg = p.rowoff[row], end = p.rowoff[row + 1];
-        for (int cb = beg; cb < end; cb += CAP) {
-            const int cnt = min(CAP, end - cb);
-            const int nt = p.r1 - p.r0;
-            auto stage = [&](int step) {  // sample warps: Y row of `step` -> buffer step % 3
-                const int r = p.r1 - 1 - step;
-                double2* xb = bufs + (step % 3) * padded_len(L2);
-                const double2* src = Y + y_index(r - p.r0, N, p.log_n2, row, 0);
-#pragma unroll
-                for (int q = 0; q < (L2 + S - 1) / S; ++q) {
-                    const int k2 = tid + q * S;
-                    if (k2 < L2) cp_async16(xb + pad16(k2), src + 2 * k2);
-                }
-                mbar_cp_async_arrive(&staged[step % 3]);
-            };
-            if (fft_warp) {
-                for (int i = 0; i < nt; ++i) {
-                    const int b = i % 3;
-                    double2* buf = bufs + b * padded_len(L2);
-                    double2 v[16];
-                    mbar_wait(&staged[b], phase[b] & 1);
-                    ++phase[b];
-                    load_stage_input<L2>(v, buf, tid);
-                    nbar_sync(BAR_FFT, G);  // all inputs read before stage 1 reuses buf
-                    block_fft_1buf<L2, -1>(v, buf, tid, T, [] { nbar_sync(BAR_FFT, G); });
-                    nbar_sync(BAR_FFT, G);  // last-stage reads of buf done
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
-                    nbar_arrive(BAR_FULL + b, ALL);
-                }
-            } else {
-                for (int i = 0; i < 3 && i < nt; ++i) stage(i);
-                // samples: h and t2 into TMEM, accumulators in registers
-                const double dn = (double)p.n;
-                double2 acc[Q];
-#pragma unroll
-                for (int k = 0; k < Q / 4; ++k) {
-                    double h[4];
-                    int t2[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int q = 4 * k + u;
-                        acc[q] = make_double2(0.0, 0.0);
-                        const int i = tid + q * S;
-                        h[u] = 0.0;
-                        t2[u] = 0;
-                        if (i < cnt) sample_geom(p, cb + i, t2[u], h[u]);
-                    }
-                    tm_st4(tcol + 8 * k, lo32(h[0]), hi32(h[0]), lo32(h[1]), hi32(h[1]));
-                    tm_st4(tcol + 8 * k + 4, lo32(h[2]), hi32(h[2]), lo32(h[3]), hi32(h[3]));
-                    tm_st4(tcol + 2 * Q + 4 * k, (unsigned)t2[0], (unsigned)t2[1], (unsigned)t2[2], (unsigned)t2[3]);
-                }
-                tm_wait_st();
-                for (int i = 0; i < nt; ++i) {
-                    const int r = p.r1 - 1 - i;
-                    const int b = i % 3;
-                    const double2* xb = bufs + b * padded_len(L2);
-                    nbar_sync(BAR_FULL + b, ALL);
-                    const double* a = kBes + r * kSeriesTerms;
-                    const int deg = p.deg[r];
-#pragma unroll
-                    for (int k = 0; k < Q / 4; ++k) {
-                        unsigned e[12];
-                        tm_ld4(tcol + 8 * k, e[0], e[1], e[2], e[3]);
-                        tm_ld4(tcol + 8 * k + 4, e[4], e[5], e[6], e[7]);
-                        tm_ld4(tcol + 2 * Q + 4 * k, e[8], e[9], e[10], e[11]);
-                        tm_wait_ld();
-                        double h[4], w[4], g[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            h[u] = mk64(e[2 * u], e[2 * u + 1]);
-                            w[u] = h[u] * h[u];
-                        }
-                        if constexpr (UNIFORM) {
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) acc[4 * k + u] = xb[e[8 + u]];
-                        } else {
-                            series_deg<4>(g, w, a, deg);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int q = 4 * k + u;
-                                const double2 X = xb[e[8 + u]];
-                                const double ax = acc[q].x;
-                                acc[q].x = __fma_rn(g[u], X.x, -h[u] * acc[q].y);
-                                acc[q].y = __fma_rn(g[u], X.y, h[u] * ax);
-                            }
-                        }
-                    }
-                    if (i + 3 < nt) {
-                        nbar_sync(BAR_SMP, S);  // every sample warp is done gathering from b
-                        stage(i + 3);
-                    }
-                }
-                // f[perm] = 2 exp(2ih) (ih)^r0 acc
-#pragma unroll
-                for (int k = 0; k < Q / 4; ++k) {
-                    unsigned e[8];
-                    tm_ld4(tcol + 8 * k, e[0], e[1], e[2], e[3]);
-                    tm_ld4(tcol + 8 * k + 4, e[4], e[5], e[6], e[7]);
-                    tm_wait_ld();
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int q = 4 * k + u;
-                        const int i = tid + q * S;
-                        if (i >= cnt) continue;
-                        double2 out = acc[q];
-                        if constexpr (!UNIFORM) {
-                            const double h = mk64(e[2 * u], e[2 * u + 1]);
-                            if (p.r0 > 0) {
-                                double hr = 1.0;
-                                for (int m = 0; m < p.r0; ++m) hr *= h;
-                                out = cscale(out, hr);
-                                switch (p.r0 & 3) {
-                                    case 1: out = make_double2(-out.y, out.x); break;
-                                    case 2: out = make_double2(-out.x, -out.y); break;
-                                    case 3: out = make_double2(out.y, -out.x); break;
-                                    default: break;
-                                }
-                            }
-                            double sn, cs;
-                            sincos(2.0 * h, &sn, &cs);
-                            out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
-                        }
-                        __stcs(f + p.perm[cb + i], out);
-                    }
-                }
-            }
-            __syncthreads();  // buffers free for the next chunk
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == G / 32) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"((unsigned)W::TM_COLS)
-                     : "memory");
     }
 }
 
@@ -1040,14 +762,7 @@ struct G2Shape {
 // instead of four plus one before the X write): each thread writes its X
 // values into the buffer slots it read last (fft2l_slot), and samples store
 // their gather slot fft2l_slot_of(t2) in TMEM instead of t2.
-//
-// CONT: one continuous step sequence over all (row, chunk) units of the CTA
-// (global step S: buffer S % 3, FFT group S % 2) instead of a CTA barrier
-// after every unit, so the FFT groups run up to three steps into the next row
-// while the sample warps finish the last Horner steps, write f and set up the
-// next row's samples.  The groups end with the EMPTY waits of three virtual
-// steps so every sample arrival is matched.
-template <int L2, bool UNIFORM, bool DSRC, int SWG, bool F2L = false, bool CONT = false>
+template <int L2, bool UNIFORM, bool DSRC, int SWG, bool F2L = false>
 __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     k2_pass2_g2(const double2* __restrict__ Y, double2* __restrict__ f, Pass2Params p) {
     static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
@@ -1082,10 +797,8 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
     const unsigned tl = tm_lane_base(tmem_base) +
                         (unsigned)(role == 2 ? (tid >> 7) * W::COLS : 0);
     const long long N = p.n;
-    const long long n1 = 1ll << p.log_n1;
     const long long n2 = 1ll << p.log_n2;
-    int S0 = 0;  // CONT: global index of the unit's first step
-    for (long long row = blockIdx.x; row < n1; row += gridDim.x) {
+    for (long long row = p.row0 + blockIdx.x; row < p.row1; row += gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         for (int cb = beg; cb < end; cb += CAP) {
             const int cnt = min(CAP, end - cb);
@@ -1093,9 +806,8 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
             if (role < 2) {
                 const int bar = BAR_GRP + role;
                 auto gsync = [bar] { nbar_sync(bar, G); };
-                const int boff = CONT ? S0 % 3 : 0;
-                for (int i = CONT ? ((role - S0) & 1) : role; i < nt; i += 2) {
-                    const int b = (i + boff) % 3;
+                for (int i = role; i < nt; i += 2) {
+                    const int b = i % 3;
                     double2* buf = bufs + b * padded_len(L2);
                     const int rr = p.r1 - 1 - i - p.r0;
                     if (tid == 0 && i + 2 < nt) {  // warm L2 with this group's next row
@@ -1105,21 +817,16 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                     const double2* row_in = Y + y_index(rr, N, p.log_n2, row, 0);
                     double2 v[16];
-                    if (p.ablate & 4) {  // diagnostics: no Y loads
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) v[q] = make_double2(tid * 1e-3 + q, i * 1e-3);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
-                    }
-                    if ((CONT ? S0 + i : i) >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step -3 from b done
+                    for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
+                    if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step -3 from b done
                     if constexpr (F2L) {
-                        if (!(p.ablate & 2)) block_fft_2l<-1>(v, buf, tid, T, gsync);
+                        block_fft_2l<-1>(v, buf, tid, T, gsync);
                         // X in place: each thread overwrites only the slots it read last
 #pragma unroll
                         for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
                     } else {
-                        if (!(p.ablate & 2)) block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
+                        block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                         gsync();  // last-stage reads of buf done
 #pragma unroll
                         for (int q = 0; q < 16; ++q) buf[tid + q * G] = v[q];
@@ -1186,10 +893,9 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                 }
                 tm_wait_st();
-                const int boff = CONT ? S0 % 3 : 0;
                 for (int i = 0; i < nt; ++i) {
                     const int r = p.r1 - 1 - i;
-                    const int b = (i + boff) % 3;
+                    const int b = i % 3;
                     const double2* xb = bufs + b * padded_len(L2);
                     nbar_sync(BAR_FULL + b, PAIR);
                     const double* a = kBes + r * kSeriesTerms;
@@ -1198,7 +904,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     (void)deg;
                     const double rd = (double)r;
 #pragma unroll 1
-                    for (int k = 0; k < ((p.ablate & 1) ? 0 : Q / CH); ++k) {
+                    for (int k = 0; k < Q / CH; ++k) {
                         unsigned av[4 * CH], gv[4 * CH], hv[2 * CH], t2v[CH];
                         tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
                         tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
@@ -1235,7 +941,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     }
                     // release b only to a later step (an EMPTY arrival nobody waits
                     // for would pair with the next use of the barrier)
-                    if (CONT || i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
+                    if (i + 3 < nt) nbar_arrive(BAR_EMPTY + b, PAIR);
                 }
                 tm_wait_st();
                 // f[perm] = 2 exp(2ih) (ih)^r0 acc
@@ -1268,21 +974,12 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                             sincospi(-mk64(dv[2 * u], dv[2 * u + 1]), &sn, &cs);
                             out = cmul(make_double2(2.0 * cs, 2.0 * sn), out);
                         }
-                        __stcs(f + p.perm[cb + i], out);
+                        __stcs(f + out_index(p, cb + i), out);
                     }
                 }
             }
-            if constexpr (CONT) {
-                S0 += nt;
-            } else {
-                __syncthreads();  // buffers and TMEM state free for the next chunk
-            }
+            __syncthreads();  // buffers and TMEM state free for the next chunk
         }
-    }
-    if constexpr (CONT) {  // match the sample warps' EMPTY arrivals of the last three steps
-        if (role < 2)
-            for (int sv = S0; sv < S0 + 3; ++sv)
-                if ((sv & 1) == role && sv >= 3) nbar_sync(BAR_EMPTY + sv % 3, PAIR);
     }
     tm_fence_before();
     __syncthreads();
@@ -1308,6 +1005,11 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
 // Sample slot j of thread t is unit sample t + 256 j; its state lives in the
 // thread's TMEM lane (shared by the same t of both groups), 13 columns:
 // acc (4), g_r, g_{r+1} (4), h (2), gather slot (1), delta (2).
+// L2 prefetch distance of k2_pass2_fs, in steps of the group (2 measured best:
+// 2.32 -> 2.21 ms; 3: 2.26, 4: 2.33).  Only even rows prefetch: the row pair
+// (t1, t1 ^ 1) shares its 128 KiB range (y_index).
+constexpr int kFsL2Prefetch = 2;
+
 struct FsShape {
     static constexpr int G = 256;
     static constexpr int SLOTS = 18;  // CAP = 4608 = 1.125 x 4096 samples per unit
@@ -1336,19 +1038,6 @@ __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int 
     gsync();  // X complete
 }
 
-// diagnostics: clock64 stamps of CTA 0 (thread 0 of each group, steps < 64) when
-// built with -DNB_FS_TRACE and run with NUFFT_TRACE_PASS2=1 (the predicated stores
-// cost ~10 % of pass 2, so they are compiled out by default)
-#ifdef NB_FS_TRACE
-#define FS_TRACE(step, e)                                                                       \
-    do {                                                                                        \
-        if (p.trace && blockIdx.x == 0 && tid == 0 && (step) < 64) p.trace[8 * (step) + (e)] = clock64(); \
-    } while (0)
-#else
-#define FS_TRACE(step, e) \
-    do {                  \
-    } while (0)
-#endif
 
 template <bool UNIFORM, bool DSRC>
 __global__ void __launch_bounds__(512, 1)
@@ -1373,7 +1062,6 @@ __global__ void __launch_bounds__(512, 1)
     const int gbar = BAR_G + grp;
     auto gsync = [gbar] { nbar_sync(gbar, G); };
     const long long N = p.n;
-    const long long n1 = 1ll << p.log_n1;
     const int nt = p.r1 - p.r0;
     const double dn = (double)p.n;
 
@@ -1484,7 +1172,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const int i = tid + (CH * (grp + 2 * kk) + u) * G;
-                pm[CH * kk + u] = i < cnt ? p.perm[cb + i] : 0;
+                pm[CH * kk + u] = i < cnt ? out_index(p, cb + i) : 0;
             }
 #pragma unroll
         for (int kk = 0; kk < KMAX; ++kk) {
@@ -1526,7 +1214,8 @@ __global__ void __launch_bounds__(512, 1)
     // one is still writing out)
     auto nchunks = [](int c) { return ((c + G - 1) / G + CH - 1) / CH; };
     // first unit of the CTA
-    long long row = blockIdx.x;
+    const long long n1 = p.row1;  // end of this launch's row range
+    long long row = p.row0 + blockIdx.x;
     int cb = 0, cnt = 0;
     auto seek = [&](long long r, int c) {  // first non-empty unit at or after (row r, sample c)
         for (; r < n1; r += gridDim.x) {
@@ -1569,18 +1258,16 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = (grp - S0) & 1; i < nt; i += 2) {
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
-            FS_TRACE(S0 + i, 0);
             if (i > 0 || !pre) {
                 if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
             }
-            FS_TRACE(S0 + i, 1);
             // this group's next row (step i + 2) is in flight during the update; a later
-            // one (step i + 2 l2pf) is warmed in L2
+            // one (step i + 2 kFsL2Prefetch) is warmed in L2
             have = i + 2 < nt;
             if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
-            if (p.l2pf && tid == 0 && i + 2 * p.l2pf < nt && (p.l2pf_pair == 0 || (urow & 1) == 0)) {
-                const void* nxt = Y + y_index(rr - 2 * p.l2pf, N, p.log_n2, urow, 0);
+            if (tid == 0 && i + 2 * kFsL2Prefetch < nt && (urow & 1) == 0) {
+                const void* nxt = Y + y_index(rr - 2 * kFsL2Prefetch, N, p.log_n2, urow, 0);
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
                              "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
             }
@@ -1588,7 +1275,6 @@ __global__ void __launch_bounds__(512, 1)
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
                 tm_fence_after();
             }
-            FS_TRACE(S0 + i, 2);
             const double rd = (double)r;
 #pragma unroll 1
             for (int k = 0; k < nch; ++k) {
@@ -1628,7 +1314,6 @@ __global__ void __launch_bounds__(512, 1)
             }
             tm_wait_st();
             tm_fence_before();
-            FS_TRACE(S0 + i, 3);
             if (i < last) nbar_arrive(BAR_H + grp, 2 * G);  // hand off step i+1
             else nbar_arrive(BAR_E, 2 * G);                   // unit's last update done
         }
@@ -1644,12 +1329,9 @@ __global__ void __launch_bounds__(512, 1)
             nbar_sync(BAR_E, 2 * G);
             tm_fence_after();
         }
-        FS_TRACE(S0 + last, 4 + grp);
         epi_half(ucb, ucnt);
-        FS_TRACE(S0 + last + 1, 4 + grp);
         if (has_next) {
             init_half(cb, cnt);
-            FS_TRACE(S0 + last, 6 + grp);
             tm_wait_st();
             tm_fence_before();
             nbar_sync(BAR_U, 2 * G);  // next unit's samples set up by both groups
@@ -1663,15 +1345,29 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 // ------------------------------------------------------------------ launch
+// Kernel choice per size (measured at N = 2^24, K = 20):
+//   pass 1: L1 = 4096 (non-uniform) k2_pass1_tma; L1 = 4096 uniform and
+//           L1 = 2048 k2_pass1_tm (two column workers, TMEM state; two-level
+//           FFT at 4096); L1 < 2048 k2_pass1.
+//   pass 2: L2 = 4096 (non-uniform) k2_pass2_fs; L2 = 4096 uniform and
+//           L2 = 2048 k2_pass2_g2 (two FFT groups + a sample warpgroup);
+//           L2 = 1024 k2_pass2_ws; L2 < 1024 k2_pass2_small.
+// (A uniform plan — K = 1, e.g. the size-2N FFTs of the inverse — has one
+// step per row, so the fused-sample kernel would be all unit boundary: 2.39
+// vs 1.23 ms per CG iteration; the warp-specialized kernel overlaps those.)
 template <int L>
 constexpr size_t pass1_smem() {
     return sizeof(double2) * (L + 2 * padded_len(L) + 16 + FftShapeX<L>::TW_LEN);
 }
-template <int L, int X2 = 2>
-constexpr size_t pass2_smem() {
-    constexpr int cap = (L >= 1024) ? WsShape<L, X2>::CAP : kMaxSamplesPerThread * (L / 16);
+template <int L>
+constexpr size_t pass2_small_smem() {
     return sizeof(double2) * (2 * padded_len(L) + FftShapeX<L>::TW_LEN) +
-           (sizeof(double) + sizeof(int)) * cap;
+           (sizeof(double) + sizeof(int)) * kMaxSamplesPerThread * (L / 16);
+}
+template <int L>
+constexpr size_t pass2_ws_smem() {
+    return sizeof(double2) * (2 * padded_len(L) + FftShapeX<L>::TW_LEN) +
+           (sizeof(double) + sizeof(int)) * WsShape<L>::CAP;
 }
 
 template <class F>
@@ -1685,49 +1381,34 @@ int occupancy(const void* fn, int threads, size_t smem) {
     return std::max(1, n);
 }
 
-inline int pass1_variant() {
-    static const int v = [] {
-        const char* e = getenv("NUFFT_PASS1_VARIANT");
-        return e ? atoi(e) : 3;
-    }();
-    return v;
-}
-
 template <int L1>
 void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int r1,
                   cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
-    if constexpr (L1 >= 2048) {
-        if (pass1_variant() >= 1) {
-            constexpr size_t SMT = P1TmShape<L1>::SMEM;
-            Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
-            auto fn = pl.uniform ? k2_pass1_tm<L1, true> : k2_pass1_tm<L1, false>;
-            if constexpr (L1 == 4096) {
-                if (pass1_variant() == 3 && !pl.uniform && pl.bk.log_n1 == 12) {
-                    CUtensorMap map;
-                    if (make_y_tensor_map(&map, Y, pl.bk.log_n2, r1 - r0)) {
-                        auto ft = k2_pass1_tma;
-                        set_smem(ft, SMT);
-                        const long long n2 = 1ll << pl.bk.log_n2;
-                        const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
-                        ft<<<grid, 512, SMT, s>>>(c, map, p);
-                        NB_LAUNCH();
-                        return;
-                    }
-                }
-                if (pass1_variant() >= 2) fn = pl.uniform ? k2_pass1_tm<L1, true, true> : k2_pass1_tm<L1, false, true>;
-            }
-            set_smem(fn, SMT);
-            const long long n2 = 1ll << pl.bk.log_n2;
-            const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
-            fn<<<grid, P1TmShape<L1>::THREADS, SMT, s>>>(c, Y, p);
-            NB_LAUNCH();
-            return;
-        }
-    }
-    constexpr size_t SM = pass1_smem<L1>();
     Pass1Params p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
     const long long n2 = 1ll << pl.bk.log_n2;
+    if constexpr (L1 >= 2048) {
+        constexpr size_t SMT = P1TmShape<L1>::SMEM;
+        const int grid = (int)std::min<long long>((n2 + 1) / 2, (long long)ctx.sms);
+        if constexpr (L1 == 4096) {
+            if (!pl.uniform) {
+                CUtensorMap map;
+                if (!make_y_tensor_map(&map, Y, pl.bk.log_n2, r1 - r0))
+                    throw Error(kCudaError, "cuTensorMapEncodeTiled failed for the pass-1 Y map");
+                set_smem(k2_pass1_tma, SMT);
+                k2_pass1_tma<<<grid, 512, SMT, s>>>(c, map, p);
+                NB_LAUNCH();
+                return;
+            }
+        }
+        constexpr bool F2L = L1 == 4096;
+        auto fn = pl.uniform ? k2_pass1_tm<L1, true, F2L> : k2_pass1_tm<L1, false, F2L>;
+        set_smem(fn, SMT);
+        fn<<<grid, P1TmShape<L1>::THREADS, SMT, s>>>(c, Y, p);
+        NB_LAUNCH();
+        return;
+    }
+    constexpr size_t SM = pass1_smem<L1>();
     auto fn = pl.uniform ? k2_pass1<L1, true> : k2_pass1<L1, false>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n2, (long long)ctx.sms * occupancy((const void*)fn, L1 / 16, SM));
@@ -1735,98 +1416,40 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
     NB_LAUNCH();
 }
 
-// pass-2 organization for rows >= 1024; NUFFT_PASS2_VARIANT selects one for
-// experiments.  Measured on B200 at N = 2^24, K = 20 (pass-2 ms):
-//   0: one FFT group, X2=2 sample width             3.36
-//   1: as 0, Y rows staged by the sample warps      3.87
-//   2: one FFT group, X2=3                          3.23
-//   3: as 2, staged                                 3.81
-//   4: one FFT group, TMEM sample metadata, 3 bufs  3.37
-//   5: two FFT groups, TMEM sample state, Bessel
-//      backward recurrence (L2 >= 2048)             3.05 (2.71 with the 2l FFT)
-//   6: fused samples (L2 = 4096, k2_pass2_fs; others fall back to 5) [default]
-inline int pass2_variant() {
-    static const int v = [] {
-        const char* e = getenv("NUFFT_PASS2_VARIANT");
-        return e ? atoi(e) : 6;
-    }();
-    return v;
-}
-
-// NUFFT_PASS2_FFT2L=0 selects the three-stage block FFT in the default pass-2
-// kernel (A/B switch for the two-level FFT)
-// NUFFT_PASS2_CONT=1: continuous steps in variant 5 (measured slower: 2.89 vs 2.71 ms, ptxas spills)
-inline bool pass2_cont() {
-    static const bool v = [] {
-        const char* e = getenv("NUFFT_PASS2_CONT");
-        return e ? atoi(e) != 0 : false;
-    }();
-    return v;
-}
-inline bool pass2_fft2l() {
-    static const bool v = [] {
-        const char* e = getenv("NUFFT_PASS2_FFT2L");
-        return e ? atoi(e) != 0 : true;
-    }();
-    return v;
-}
-
-template <int L2, bool UNIFORM, int X2, bool STAGE>
-void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms,
-               cudaStream_t s) {
-    constexpr size_t SM = pass2_smem<L2, X2>();
-    constexpr int threads = WsShape<L2, X2>::ALL;
-    auto fn = k2_pass2_ws<L2, UNIFORM, X2, STAGE>;
+template <int L2, bool UNIFORM>
+void launch_ws(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    constexpr size_t SM = pass2_ws_smem<L2>();
+    constexpr int threads = WsShape<L2>::ALL;
+    auto fn = k2_pass2_ws<L2, UNIFORM>;
     set_smem(fn, SM);
     const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
     fn<<<grid, threads, SM, s>>>(Y, f, p);
-    NB_LAUNCH();
-}
-
-template <int L2, bool UNIFORM, int SWG = 1>
-void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
-    constexpr size_t SM = G2Shape<L2, SWG>::SMEM;
-    constexpr int threads = G2Shape<L2, SWG>::ALL;
-    auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG> : k2_pass2_g2<L2, UNIFORM, false, SWG>;
-    if constexpr (L2 == 4096) {
-        if (pass2_fft2l() && pass2_cont())
-            fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG, true, true> : k2_pass2_g2<L2, UNIFORM, false, SWG, true, true>;
-        else if (pass2_fft2l())
-            fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, SWG, true> : k2_pass2_g2<L2, UNIFORM, false, SWG, true>;
-    }
-    set_smem(fn, SM);
-    const int grid = (int)std::min<long long>(n1, (long long)sms);
-    fn<<<grid, threads, SM, s>>>(Y, f, p);
-    NB_LAUNCH();
-}
-
-template <bool UNIFORM>
-void launch_fs(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
-    // NUFFT_FS_EXTRA_SMEM (KiB, diagnostics): launch with more shared memory than needed,
-    // i.e. a smaller L1 carve-out (this kernel is sensitive to it)
-    static const int extra_kb = getenv("NUFFT_FS_EXTRA_SMEM") ? atoi(getenv("NUFFT_FS_EXTRA_SMEM")) : 0;
-    const size_t SM = std::min<size_t>(227 * 1024, FsShape::SMEM + 1024 * (size_t)extra_kb);
-    auto fn = p.ds ? k2_pass2_fs<UNIFORM, true> : k2_pass2_fs<UNIFORM, false>;
-    set_smem(fn, SM);
-    const int grid = (int)std::min<long long>(n1, (long long)sms);
-    fn<<<grid, 2 * FsShape::G, SM, s>>>(Y, f, p);
     NB_LAUNCH();
 }
 
 template <int L2, bool UNIFORM>
-void launch_tm(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
-    constexpr size_t SM = TmShape<L2>::SMEM;
-    constexpr int threads = TmShape<L2>::ALL;
-    auto fn = k2_pass2_tm<L2, UNIFORM>;
+void launch_g2(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    constexpr size_t SM = G2Shape<L2>::SMEM;
+    constexpr int threads = G2Shape<L2>::ALL;
+    constexpr bool F2L = L2 == 4096;
+    auto fn = p.ds ? k2_pass2_g2<L2, UNIFORM, true, 1, F2L> : k2_pass2_g2<L2, UNIFORM, false, 1, F2L>;
     set_smem(fn, SM);
-    const int grid = (int)std::min<long long>(n1, (long long)sms * occupancy((const void*)fn, threads, SM));
+    const int grid = (int)std::min<long long>(n1, (long long)sms);
     fn<<<grid, threads, SM, s>>>(Y, f, p);
     NB_LAUNCH();
 }
 
+void launch_fs(const double2* Y, double2* f, const Pass2Params& p, long long n1, int sms, cudaStream_t s) {
+    auto fn = p.ds ? k2_pass2_fs<false, true> : k2_pass2_fs<false, false>;
+    set_smem(fn, FsShape::SMEM);
+    const int grid = (int)std::min<long long>(n1, (long long)sms);
+    fn<<<grid, 2 * FsShape::G, FsShape::SMEM, s>>>(Y, f, p);
+    NB_LAUNCH();
+}
+
 template <int L2>
-void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int r1,
-                  cudaStream_t s) {
+void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int r1, long long row0,
+                  long long row1, bool sorted_out, cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     Pass2Params p{};
     p.n = (long long)pl.n;
@@ -1837,85 +1460,30 @@ void launch_pass2(const double2* Y, double2* f, const CorePlan& pl, int r0, int 
     p.xs = pl.bk.xs.as<double>();
     p.ds = pl.delta_from_freq ? pl.bk.ds.as<double>() : nullptr;
     p.skey = pl.delta_from_freq ? pl.bk.skey.as<unsigned>() : nullptr;
-    p.perm = pl.bk.perm.as<int>();
+    p.perm = sorted_out ? nullptr : pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
+    p.row0 = row0;
+    p.row1 = row1;
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
     p.deg_rel0 = bessel_series_degree_rel(pl.gamma_factors, r1 - 1);
     p.deg_rel1 = bessel_series_degree_rel(pl.gamma_factors, r1);
-    static const bool trace = getenv("NUFFT_TRACE_PASS2") != nullptr;
-    static const int ablate = getenv("NUFFT_ABLATE") ? atoi(getenv("NUFFT_ABLATE")) : 0;
-    p.ablate = ablate;
-    // NUFFT_FS_L2PF = k: L2 prefetch of the group's row k steps ahead (0: off)
-    static const int l2pf = getenv("NUFFT_FS_L2PF") ? atoi(getenv("NUFFT_FS_L2PF")) : 2;
-    p.l2pf = l2pf;
-    static const int l2pf_pair = getenv("NUFFT_FS_L2PF_PAIR") ? atoi(getenv("NUFFT_FS_L2PF_PAIR")) : 1;
-    p.l2pf_pair = l2pf_pair;
-    unsigned long long* tr = nullptr;
-    if (trace) {
-        NB_CUDA(cudaMalloc(&tr, 8 * 8 * 64));
-        NB_CUDA(cudaMemset(tr, 0, 8 * 8 * 64));
+    const long long n1 = row1 - row0;  // rows of this launch (grid size)
+    const bool u = pl.uniform;
+    if constexpr (L2 == 4096) {
+        if (!u) return launch_fs(Y, f, p, n1, ctx.sms, s);
     }
-    p.trace = tr;
-    const long long n1 = 1ll << pl.bk.log_n1;
-    if constexpr (L2 >= 1024) {
-        const bool u = pl.uniform;
-        switch (pass2_variant()) {
-            case 1: u ? launch_ws<L2, true, 2, true>(Y, f, p, n1, ctx.sms, s)
-                      : launch_ws<L2, false, 2, true>(Y, f, p, n1, ctx.sms, s); break;
-            case 2: u ? launch_ws<L2, true, 3, false>(Y, f, p, n1, ctx.sms, s)
-                      : launch_ws<L2, false, 3, false>(Y, f, p, n1, ctx.sms, s); break;
-            case 3: u ? launch_ws<L2, true, 3, true>(Y, f, p, n1, ctx.sms, s)
-                      : launch_ws<L2, false, 3, true>(Y, f, p, n1, ctx.sms, s); break;
-            case 4: u ? launch_tm<L2, true>(Y, f, p, n1, ctx.sms, s)
-                      : launch_tm<L2, false>(Y, f, p, n1, ctx.sms, s); break;
-            case 6:
-                // (a uniform plan — K = 1, e.g. the size-2N FFTs of the inverse — has one step per
-                // row, so the fused kernel would be all unit boundary: 2.39 vs 1.23 ms per CG
-                // iteration; the warp-specialized kernel overlaps those)
-                if constexpr (L2 == 4096) {
-                    if (!u) {
-                        launch_fs<false>(Y, f, p, n1, ctx.sms, s);
-                        break;
-                    }
-                }
-                [[fallthrough]];
-            case 5:
-                if constexpr (L2 >= 2048) {
-                    u ? launch_g2<L2, true>(Y, f, p, n1, ctx.sms, s) : launch_g2<L2, false>(Y, f, p, n1, ctx.sms, s);
-                } else {
-                    u ? launch_ws<L2, true, 3, false>(Y, f, p, n1, ctx.sms, s)
-                      : launch_ws<L2, false, 3, false>(Y, f, p, n1, ctx.sms, s);
-                }
-                break;
-            default: u ? launch_ws<L2, true, 2, false>(Y, f, p, n1, ctx.sms, s)
-                       : launch_ws<L2, false, 2, false>(Y, f, p, n1, ctx.sms, s); break;
-        }
+    if constexpr (L2 >= 2048) {
+        u ? launch_g2<L2, true>(Y, f, p, n1, ctx.sms, s) : launch_g2<L2, false>(Y, f, p, n1, ctx.sms, s);
+    } else if constexpr (L2 == 1024) {
+        u ? launch_ws<L2, true>(Y, f, p, n1, ctx.sms, s) : launch_ws<L2, false>(Y, f, p, n1, ctx.sms, s);
     } else {
-        constexpr size_t SM = pass2_smem<L2>();
+        constexpr size_t SM = pass2_small_smem<L2>();
         constexpr int threads = L2 / 16;
-        auto fn = pl.uniform ? k2_pass2_small<L2, true> : k2_pass2_small<L2, false>;
+        auto fn = u ? k2_pass2_small<L2, true> : k2_pass2_small<L2, false>;
         set_smem(fn, SM);
         const int grid = (int)std::min<long long>(n1, (long long)ctx.sms * occupancy((const void*)fn, threads, SM));
         fn<<<grid, threads, SM, s>>>(Y, f, p);
         NB_LAUNCH();
-    }
-    if (tr) {
-        unsigned long long h[8 * 64];
-        NB_CUDA(cudaStreamSynchronize(s));
-        NB_CUDA(cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost));
-        const unsigned long long t0 = h[0];
-        if (pass2_variant() == 6 && L2 == 4096 && !pl.uniform) {  // k2_pass2_fs (-DNB_FS_TRACE build)
-            for (int i = 0; i < 64; ++i)
-                fprintf(stderr, "fs S=%2d grp %d fft[%7lld %7lld] upd[%7lld %7lld] bnd[epi %7lld %7lld init %7lld %7lld]\n", i, i & 1,
-                        (long long)(h[8 * i] - t0), (long long)(h[8 * i + 1] - t0), (long long)(h[8 * i + 2] - t0),
-                        (long long)(h[8 * i + 3] - t0), (long long)(h[8 * i + 4] - t0), (long long)(h[8 * i + 5] - t0),
-                        (long long)(h[8 * i + 6] - t0), (long long)(h[8 * i + 7] - t0));
-        } else
-        for (int i = 0; i < r1 - r0; ++i)
-            fprintf(stderr, "trace i=%2d fft[start %7lld input %7lld done %7lld]  smp[full %7lld horner %7lld staged %7lld]\n", i,
-                    (long long)(h[8 * i] - t0), (long long)(h[8 * i + 1] - t0), (long long)(h[8 * i + 2] - t0),
-                    (long long)(h[8 * i + 4] - t0), (long long)(h[8 * i + 5] - t0), (long long)(h[8 * i + 6] - t0));
-        cudaFree(tr);
     }
 }
 
@@ -1935,17 +1503,18 @@ void dispatch_pass1(int L, const double2* c, double2* Y, const CorePlan& pl, int
     }
 }
 void dispatch_pass2(int L, const double2* Y, double2* f, const CorePlan& pl, int r0, int r1,
-                    cudaStream_t s) {
+                    cudaStream_t s, long long row0 = 0, long long row1 = -1, bool sorted_out = false) {
+    if (row1 < 0) row1 = 1ll << pl.bk.log_n1;
     switch (L) {
-        case 16: return launch_pass2<16>(Y, f, pl, r0, r1, s);
-        case 32: return launch_pass2<32>(Y, f, pl, r0, r1, s);
-        case 64: return launch_pass2<64>(Y, f, pl, r0, r1, s);
-        case 128: return launch_pass2<128>(Y, f, pl, r0, r1, s);
-        case 256: return launch_pass2<256>(Y, f, pl, r0, r1, s);
-        case 512: return launch_pass2<512>(Y, f, pl, r0, r1, s);
-        case 1024: return launch_pass2<1024>(Y, f, pl, r0, r1, s);
-        case 2048: return launch_pass2<2048>(Y, f, pl, r0, r1, s);
-        case 4096: return launch_pass2<4096>(Y, f, pl, r0, r1, s);
+        case 16: return launch_pass2<16>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 32: return launch_pass2<32>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 64: return launch_pass2<64>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 128: return launch_pass2<128>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 256: return launch_pass2<256>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 512: return launch_pass2<512>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 1024: return launch_pass2<1024>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 2048: return launch_pass2<2048>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
+        case 4096: return launch_pass2<4096>(Y, f, pl, r0, r1, row0, row1, sorted_out, s);
         default: throw Error(kInternal, "pass2 size");
     }
 }
@@ -1978,6 +1547,34 @@ __global__ void k2g_accum(const double2* __restrict__ X, double2* __restrict__ f
 inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
+
+namespace {
+__global__ void k_unpermute(const double2* __restrict__ fs, const int* __restrict__ perm, long long n,
+                            double2* __restrict__ f) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) __stcs(f + perm[i], __ldcs(fs + i));
+}
+}  // namespace
+
+void exec_type2_pass1(const CorePlan& pl, const double2* c, double2* Y, size_t r0, size_t r1,
+                      cudaStream_t s) {
+    if (!pl.fused || pl.bk.log_n1 == 0) throw Error(kInternal, "exec_type2_pass1: fused plan with N1 > 1 only");
+    ensure_bessel_constants(pl.device);
+    dispatch_pass1(1 << pl.bk.log_n1, c, Y, pl, (int)r0, (int)r1, s);
+}
+void exec_type2_pass2_rows(const CorePlan& pl, const double2* Y, double2* f, size_t r0, size_t r1,
+                           long long row0, long long row1, bool sorted_out, cudaStream_t s) {
+    if (!pl.fused || pl.bk.log_n1 == 0) throw Error(kInternal, "exec_type2_pass2_rows: fused plan with N1 > 1 only");
+    if (row1 <= row0) return;
+    dispatch_pass2(1 << pl.bk.log_n2, Y, f, pl, (int)r0, (int)r1, s, row0, row1, sorted_out);
+}
+void unpermute(const CorePlan& pl, const double2* fs, double2* f, size_t batch, cudaStream_t s) {
+    for (size_t b = 0; b < batch; ++b) {
+        k_unpermute<<<blocks(pl.n), 256, 0, s>>>(fs + b * pl.n, pl.bk.perm.as<int>(), (long long)pl.n,
+                                                 f + b * pl.n);
+        NB_LAUNCH();
+    }
+}
 
 void exec_type2(const CorePlan& pl, const double2* c, double2* f, size_t batch, size_t r0,
                 size_t r1, cudaStream_t s, cudaEvent_t* ev) {

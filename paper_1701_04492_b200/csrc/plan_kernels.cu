@@ -323,6 +323,9 @@ void build_buckets(CorePlan& p, cudaStream_t s) {
     k_bucket_offsets<unsigned><<<blocks(n + 1), 256, 0, s>>>(
         keys_out.as<unsigned>(), (long long)n, log_n2, (long long)n1, p.bk.rowoff.as<int>());
     NB_LAUNCH();
+    p.bk.rowoff_host.resize(n1 + 1);  // row ranges -> sample ranges on the host (multi-GPU chunking)
+    NB_CUDA(cudaMemcpyAsync(p.bk.rowoff_host.data(), p.bk.rowoff.as<int>(), 4 * (n1 + 1),
+                            cudaMemcpyDeviceToHost, s));
     p.bk.xs.alloc(8 * n);
     k_gather_x<<<blocks(n), 256, 0, s>>>(p.ax.x.as<double>(), p.bk.perm.as<int>(), (long long)n,
                                          p.bk.xs.as<double>());

@@ -41,6 +41,7 @@ struct Buckets {
     DevArray ds, skey;           // fused transpose core (type I / adjoint / III inner)
     DevArray sort_perm;          // generic transpose core: samples sorted by t (int32)
     DevArray bin_off;            // generic transpose core: N+1 offsets (int32)
+    std::vector<int> rowoff_host;  // host copy of rowoff (row chunk -> sample range)
 };
 
 // Type-I/II core plan: a sample axis, a rank, and the factor parameters.
@@ -107,6 +108,16 @@ void cheb_eval(const double* pts_dev, size_t n, size_t K, double* out_dev, cudaS
 // pass 2 (batch 1) — per-kernel timing on the launching stream for the bench
 void exec_type2(const CorePlan& p, const double2* c, double2* f, size_t batch, size_t r0,
                 size_t r1, cudaStream_t s, cudaEvent_t* ev = nullptr);
+// building blocks of the multi-GPU r-split (nufft2_multi.cu), fused plans with
+// N1 > 1 only: pass 1 of terms [r0, r1) into Y (16 (r1 - r0) N bytes), and
+// pass 2 over rows [row0, row1) writing the partial sum either to f[perm]
+// (natural order) or, sorted_out, to fs[i] in bucket order (rowoff ranges)
+void exec_type2_pass1(const CorePlan& p, const double2* c, double2* Y, size_t r0, size_t r1,
+                      cudaStream_t s);
+void exec_type2_pass2_rows(const CorePlan& p, const double2* Y, double2* f, size_t r0, size_t r1,
+                           long long row0, long long row1, bool sorted_out, cudaStream_t s);
+// f[perm[i]] = fs[i] (bucket order -> natural order), batch vectors of N
+void unpermute(const CorePlan& p, const double2* fs, double2* f, size_t batch, cudaStream_t s);
 // F2~^T g = sum_r v_r .* F scatter_t(u_r .* g)   (transforms.hpp:206-221)
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
                     cudaStream_t s);

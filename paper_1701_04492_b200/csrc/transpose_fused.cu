@@ -829,15 +829,12 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
     if constexpr (L2 == 4096) {  // at 2048 two single-worker CTAs per SM are as good
         constexpr size_t SMT = PassATmShape<L2>::SMEM;
-        auto fnt = pl.uniform ? k1_passA_tm<L2, true> : k1_passA_tm<L2, false>;
-        static const bool f2l = !getenv("NUFFT_PASSA_FFT3");  // A/B: three-stage FFT
-        static const bool tma = !getenv("NUFFT_PASSA_NO_TMA");  // A/B: LSU row stores
+        // two-level row FFT; Z rows stored by TMA (LSU stores when the tensor map
+        // cannot describe Z)
+        auto fnt = pl.uniform ? k1_passA_tm<L2, true, true> : k1_passA_tm<L2, false, true>;
         CUtensorMap zmap{};
-        if (f2l) fnt = pl.uniform ? k1_passA_tm<L2, true, true> : k1_passA_tm<L2, false, true>;
-        if constexpr (L2 == 4096) {
-            if (f2l && tma && make_z_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
-                fnt = pl.uniform ? k1_passA_tm<L2, true, true, true> : k1_passA_tm<L2, false, true, true>;
-        }
+        if (make_z_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
+            fnt = pl.uniform ? k1_passA_tm<L2, true, true, true> : k1_passA_tm<L2, false, true, true>;
         set_smem(fnt, SMT);
         const long long rows = 1ll << pl.bk.log_n1;
         const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
@@ -862,10 +859,9 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
         CUtensorMap zmap{};
         if constexpr (L1 == 4096) {
-            static const bool f2l = !getenv("NUFFT_PASSB_FFT3");  // A/B: three-stage FFT
-            static const bool tma = !getenv("NUFFT_PASSB_NO_TMA");  // A/B: LSU column loads
-            if (f2l) fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
-            if (f2l && tma && pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0)) {
+            // two-level column FFT; Z columns loaded by TMA when N2 = 4096
+            fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
+            if (pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0)) {
                 fn = pl.uniform ? k1_passB_tm<L1, true, true, true> : k1_passB_tm<L1, false, true, true>;
                 SMT += sizeof(double2) * 2 * 2048;  // the two `pre` half-column buffers
             }

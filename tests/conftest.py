@@ -20,6 +20,39 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running (large N)")
 
 
+_FULLSIZE = {}
+
+
+def pytest_collection_modifyitems(session, config, items):
+    """Start the reference's own full-size runs (tests/fullsize_ref.py) as soon
+    as test_gpu_fullsize.py is part of the selected session, so the CPU work
+    overlaps the GPU tests that run before it."""
+    if not any("test_gpu_fullsize" in it.nodeid for it in items):
+        return
+    from oracle import pyoracle
+    if not pyoracle.available("reference"):
+        return  # the fixture reports it
+    import tempfile
+
+    import fullsize_ref
+    d = tempfile.mkdtemp(prefix="nufft_fullsize_ref_")
+    _FULLSIZE["runner"] = fullsize_ref.Runner(d)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    r = _FULLSIZE.pop("runner", None)
+    if r is not None:
+        r.close()
+
+
+@pytest.fixture(scope="session")
+def fullsize_ref_runs():
+    r = _FULLSIZE.get("runner")
+    if r is None:
+        pytest.fail("oracle/_ref/libnufft_ref.so missing: the reference's own output is the full-size oracle")
+    return r
+
+
 @pytest.fixture(scope="session")
 def port():
     from oracle import pyoracle

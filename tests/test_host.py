@@ -98,3 +98,17 @@ def test_compute_fails_loudly_without_gpu():
         nb.plan_nufft2([0.1, 0.2], 1e-12)
     with pytest.raises(nb.NufftError):
         nb.fft_forward([1, 2, 3])
+
+
+def test_sampler_bit_identical_to_reference_sampler(port):
+    """nufft_sampler_* / include/nufft/random.hpp draw the reference's
+    GaussianSampler streams (random.hpp:14-60) bit for bit — bench.py's two
+    arms and the full-size parity tests rely on it.  Host-only, no GPU."""
+    from oracle import pyoracle
+    o = pyoracle.Oracle("reference") if pyoracle.available("reference") else port
+    for seed in (0, 1, 20240, 2 ** 63 + 5):
+        a, b = nb.GaussianSampler(seed), o.sampler(seed)
+        assert np.array_equal(a.uniform_vector(1001, -0.5, 0.5), b.uniform_vector(1001, -0.5, 0.5))
+        assert np.array_equal(a.complex_vector(777), b.complex_vector(777))  # odd count: spare carried
+        assert a() == b.normal()
+        assert np.array_equal(a.uniform_vector(5, 0.0, 4096.0), b.uniform_vector(5, 0.0, 4096.0))
