@@ -962,7 +962,7 @@ int nufft_plan3_exec(const nufft_plan3* plan, const double* c_dev, double* f_dev
         NB_CUDA(cudaSetDevice(st.a.device));
         nb::exec_type3(st, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev),
                        batch, as_stream(stream));
-        nb::fft_count(st.a.n, st.kc * st.inner.K * batch);
+        nb::fft_count(st.a.n, st.a.K * st.inner.K * batch);  // the beta family needs no FFTs (exec_type3)
     });
 }
 int nufft_plan3_exec_host(const nufft_plan3* plan, const double* c, size_t len, double* f,
@@ -974,7 +974,7 @@ int nufft_plan3_exec_host(const nufft_plan3* plan, const double* c, size_t len, 
         cudaStream_t s = cudaStreamPerThread;
         host_roundtrip(c, 2 * st.a.n * batch, f, 2 * st.a.n * batch, s, [&](double2* a, double2* b) {
             nb::exec_type3(st, a, b, batch, s);
-            nb::fft_count(st.a.n, st.kc * st.inner.K * batch);
+            nb::fft_count(st.a.n, st.a.K * st.inner.K * batch);  // the beta family needs no FFTs (exec_type3)
         });
     });
 }

@@ -7,6 +7,8 @@
 // Scatter determinism: samples are pre-sorted by bin t at plan time (stable
 // radix sort keeps ascending j inside a bin), one thread sums one bin in that
 // order — no floating-point atomics.
+#include <algorithm>
+
 #include "bessel.cuh"
 #include "plans.hpp"
 
@@ -47,41 +49,119 @@ __global__ void k_conj(const double2* __restrict__ in, double2* __restrict__ out
     if (i < n) out[i] = cconj(in[i]);
 }
 
-// scaled[i] = V_q(omega_i) c[i]; V_q = v^A_r(omega/N) [* exp(-2 pi i omega) for the beta family]
+// scaled[i] = v^A_r(omega_i / N) c[i]   (the first family's V_r, transforms.hpp:337-340)
 __global__ void k3_scale(const double2* __restrict__ c, const double* __restrict__ omega,
-                         double2* __restrict__ out, long long n, int r, int phase, int uniform) {
+                         double2* __restrict__ out, long long n, int r, int uniform) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double w = omega[i];
     double vr = 1.0;
     if (!uniform) {
-        const double s = __dsub_rn(__dmul_rn(2.0, __ddiv_rn(w, (double)n)), 1.0);
+        const double s = __dsub_rn(__dmul_rn(2.0, __ddiv_rn(omega[i], (double)n)), 1.0);
         vr = v_factor_from_s(fmin(1.0, fmax(-1.0, s)), r);
     }
-    double2 v = make_double2(vr, 0.0);
-    if (phase) {
-        const double fr = w - floor(w);  // exact
-        double sn, cs;
-        sincospi(-2.0 * fr, &sn, &cs);
-        v = make_double2(vr * cs, vr * sn);
-    }
-    out[i] = cmul(v, c[i]);
+    const double2 x = c[i];
+    out[i] = make_double2(vr * x.x, vr * x.y);
 }
 
-// f[j] (+)= U_q[j] y[t_j];  U_q = u^A_r(delta_j) * (1 - beta_j | beta_j | 1)
-__global__ void k3_accum(const double2* __restrict__ y, double2* __restrict__ f,
-                         const double* __restrict__ delta, const long long* __restrict__ s,
-                         const long long* __restrict__ t, long long n, int r, int deg, int family,
-                         int first, int uniform) {
+// The beta family of a non-trivial B (transforms.hpp:355-370): only samples with
+// beta_j = 1 see it, and for those t_j = 0, so the inner type-I output is needed at
+// index 0 only, where every phase exp(-2 pi i 0 omega_k / N) is exactly 1:
+//     D_r = sum_k v^A_r(omega_k / N) exp(-2 pi i omega_k) c_k,   r < K
+// (SURVEY.md §8(a18)).  Stage 1: each block sums a strided slice of k for terms
+// [r0, r0 + 8) into part[block][r]; stage 2 adds the blocks in index order —
+// a fixed summation order, so D is bit-reproducible.
+constexpr int kDotTerms = 8;
+constexpr int kDotBlocks = 592;  // 4 x 148 SMs
+constexpr int kDotThreads = 256;
+__global__ void __launch_bounds__(kDotThreads)
+    k3_beta_dot_part(const double2* __restrict__ c, const double* __restrict__ omega, long long n, int r0,
+                     int nr, int uniform, double2* __restrict__ part) {
+    __shared__ double2 red[kDotTerms][kDotThreads];
+    double2 acc[kDotTerms];
+#pragma unroll
+    for (int q = 0; q < kDotTerms; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const double w = omega[k];
+        double sn, cs;
+        sincospi(-2.0 * (w - floor(w)), &sn, &cs);  // exp(-2 pi i omega), argument reduced exactly
+        const double2 ec = cmul(make_double2(cs, sn), c[k]);
+        // v_r for r = r0 .. r0 + nr - 1 by the recurrence from T_0, T_1
+        const double s = fmin(1.0, fmax(-1.0, __dsub_rn(__dmul_rn(2.0, __ddiv_rn(w, (double)n)), 1.0)));
+        double tm1 = 1.0, t = s;
+        for (int r = 1; r < r0; ++r) {
+            const double tn = __fma_rn(2.0 * s, t, -tm1);
+            tm1 = t;
+            t = tn;
+        }
+#pragma unroll
+        for (int q = 0; q < kDotTerms; ++q) {
+            const int r = r0 + q;
+            if (q < nr) {
+                const double vr = uniform ? 1.0 : (r == 0 ? 0.5 : t);
+                acc[q].x = __fma_rn(vr, ec.x, acc[q].x);
+                acc[q].y = __fma_rn(vr, ec.y, acc[q].y);
+                if (r >= 1) {
+                    const double tn = __fma_rn(2.0 * s, t, -tm1);
+                    tm1 = t;
+                    t = tn;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kDotTerms; ++q) red[q][threadIdx.x] = acc[q];
+    __syncthreads();
+    for (int half = kDotThreads / 2; half > 0; half >>= 1) {
+        if (threadIdx.x < half)
+#pragma unroll
+            for (int q = 0; q < kDotTerms; ++q) red[q][threadIdx.x] = cadd(red[q][threadIdx.x], red[q][threadIdx.x + half]);
+        __syncthreads();
+    }
+    if (threadIdx.x < nr) part[(long long)blockIdx.x * kDotTerms + threadIdx.x] = red[threadIdx.x][0];
+}
+__global__ void k3_beta_dot_final(const double2* __restrict__ part, int r0, int nr, double2* __restrict__ D) {
+    const int q = threadIdx.x;
+    if (q >= nr) return;
+    double2 s = make_double2(0.0, 0.0);
+    for (int b = 0; b < kDotBlocks; ++b) s = cadd(s, part[(long long)b * kDotTerms + q]);
+    D[r0 + q] = s;
+}
+
+// f[j] = sum_r u^A_r(delta_j) Z_r,j with Z_r,j = y_r[t_j] (beta_j = 0) or D_r
+// (beta_j = 1) — both families and the K per-term accumulations of the
+// reference's exec_nufft3 (transforms.hpp:386-392) in one sample-ordered pass.
+// u_r = 2 exp(2ih) (ih)^r g_r(h^2): Horner in r over acc <- acc (ih) + g_r Z_r,
+// g_r by the backward Bessel recurrence g_{r-1} = r g_r - w g_{r+1} from two
+// series values (as in the type-II pass 2, nufft2.cu).
+__global__ void k3_epilogue(const double2* __restrict__ Y, const double2* __restrict__ D,
+                            const double* __restrict__ delta, const long long* __restrict__ sv,
+                            const long long* __restrict__ tv, long long n, int K, int deg_top0, int deg_top1,
+                            int uniform, double2* __restrict__ f) {
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    double2 u = uniform ? make_double2(1.0, 0.0) : u_factor(delta[j], r, deg);
-    if (family) {  // 1: (1 - beta), 2: beta ; beta = (s - t)/N in {0, 1}
-        const double beta = (double)(s[j] - t[j]) / (double)n;
-        u = cscale(u, family == 1 ? 1.0 - beta : beta);
+    const long long t = tv[j];
+    const bool beta = sv[j] != t;  // s = N, t = 0: the node at 1 (transforms.hpp:345-350)
+    if (uniform) {
+        f[j] = beta ? D[0] : Y[t];
+        return;
     }
-    const double2 term = cmul(u, y[t[j]]);
-    f[j] = first ? term : cadd(f[j], term);
+    const double h = half_phase(delta[j]);
+    const double w = h * h;
+    double g1 = bessel_g_rt(K, deg_top1, w);      // g_K
+    double g0 = bessel_g_rt(K - 1, deg_top0, w);  // g_{K-1}
+    double2 acc = make_double2(0.0, 0.0);
+    for (int r = K - 1; r >= 0; --r) {
+        const double2 z = beta ? D[r] : __ldg(Y + (long long)r * n + t);
+        const double ax = acc.x;
+        acc.x = __fma_rn(g0, z.x, -h * acc.y);
+        acc.y = __fma_rn(g0, z.y, h * ax);
+        const double gm1 = __fma_rn((double)r, g0, -w * g1);  // g_{r-1}
+        g1 = g0;
+        g0 = gm1;
+    }
+    double sn, cs;
+    sincos(2.0 * h, &sn, &cs);
+    f[j] = cmul(make_double2(2.0 * cs, 2.0 * sn), acc);
 }
 
 }  // namespace
@@ -117,23 +197,38 @@ void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch,
     ensure_bessel_constants(p.a.device);
     const size_t N = p.a.n;
     const size_t K = p.a.K;
-    DevBuf scaled(sizeof(double2) * N, s), y(sizeof(double2) * N, s);
+    const int uni = p.a.uniform ? 1 : 0;
+    // y_r = F1~(v_r .* c) for the first family (K inner type-I transforms), kept
+    // for the single sample-ordered epilogue; the beta family reduces to K dot
+    // products (D_r) whenever B is non-trivial
+    DevBuf scaled(sizeof(double2) * N, s), Y(sizeof(double2) * N * K, s), D(sizeof(double2) * K, s);
+    DevBuf part(p.btrivial ? 16 : sizeof(double2) * kDotBlocks * kDotTerms, s);
+    const int deg0 = bessel_series_degree_rel(p.a.gamma_factors, (int)K - 1);
+    const int deg1 = bessel_series_degree_rel(p.a.gamma_factors, (int)K);
     for (size_t b = 0; b < batch; ++b) {
-        for (size_t q = 0; q < p.kc; ++q) {
-            const size_t r = q % K;
-            const bool second = q >= K;
-            k3_scale<<<blocks(N), 256, 0, s>>>(c + b * N, p.omega.as<double>(), scaled.as<double2>(),
-                                               (long long)N, (int)r, second ? 1 : 0,
-                                               p.a.uniform ? 1 : 0);
+        const double2* cb = c + b * N;
+        for (size_t r = 0; r < K; ++r) {
+            k3_scale<<<blocks(N), 256, 0, s>>>(cb, p.omega.as<double>(), scaled.as<double2>(), (long long)N,
+                                               (int)r, uni);
             NB_LAUNCH();
-            exec_transpose(p.inner, scaled.as<double2>(), y.as<double2>(), 1, s);
-            const int family = p.btrivial ? 0 : (second ? 2 : 1);
-            k3_accum<<<blocks(N), 256, 0, s>>>(y.as<double2>(), f + b * N, p.a.ax.delta.as<double>(),
-                                               p.a.ax.s.as<long long>(), p.a.ax.t.as<long long>(),
-                                               (long long)N, (int)r, p.a.series_deg[r], family,
-                                               q == 0 ? 1 : 0, p.a.uniform ? 1 : 0);
-            NB_LAUNCH();
+            exec_transpose(p.inner, scaled.as<double2>(), Y.as<double2>() + r * N, 1, s);
         }
+        if (!p.btrivial) {
+            for (size_t r0 = 0; r0 < K; r0 += kDotTerms) {
+                const int nr = (int)std::min<size_t>(kDotTerms, K - r0);
+                k3_beta_dot_part<<<kDotBlocks, kDotThreads, 0, s>>>(cb, p.omega.as<double>(), (long long)N, (int)r0,
+                                                                     nr, uni, part.as<double2>());
+                NB_LAUNCH();
+                k3_beta_dot_final<<<1, 32, 0, s>>>(part.as<double2>(), (int)r0, nr, D.as<double2>());
+                NB_LAUNCH();
+            }
+        } else {
+            NB_CUDA(cudaMemsetAsync(D.get(), 0, sizeof(double2) * K, s));
+        }
+        k3_epilogue<<<blocks(N), 256, 0, s>>>(Y.as<double2>(), D.as<double2>(), p.a.ax.delta.as<double>(),
+                                              p.a.ax.s.as<long long>(), p.a.ax.t.as<long long>(), (long long)N,
+                                              (int)K, deg0, deg1, uni, f + b * N);
+        NB_LAUNCH();
     }
 }
 

@@ -1549,10 +1549,22 @@ inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / 
 }  // namespace
 
 namespace {
-__global__ void k_unpermute(const double2* __restrict__ fs, const int* __restrict__ perm, long long n,
+// f[j] = fs[invperm[j]]: coalesced f stores and invperm loads, 16-byte gathers from fs
+// (random loads stay in flight; scattered 16-byte stores would be partial-sector
+// read-modify-writes in L2)
+__global__ void k_unpermute(const double2* __restrict__ fs, const int* __restrict__ invperm, long long n,
                             double2* __restrict__ f) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) __stcs(f + perm[i], __ldcs(fs + i));
+    const long long j0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (j0 + 3 < n) {
+        const int4 ix = __ldcs(reinterpret_cast<const int4*>(invperm + j0));
+        const double2 a = __ldg(fs + ix.x), b = __ldg(fs + ix.y), c = __ldg(fs + ix.z), d = __ldg(fs + ix.w);
+        __stcs(f + j0, a);
+        __stcs(f + j0 + 1, b);
+        __stcs(f + j0 + 2, c);
+        __stcs(f + j0 + 3, d);
+    } else {
+        for (long long j = j0; j < n; ++j) f[j] = fs[invperm[j]];
+    }
 }
 }  // namespace
 
@@ -1570,8 +1582,8 @@ void exec_type2_pass2_rows(const CorePlan& pl, const double2* Y, double2* f, siz
 }
 void unpermute(const CorePlan& pl, const double2* fs, double2* f, size_t batch, cudaStream_t s) {
     for (size_t b = 0; b < batch; ++b) {
-        k_unpermute<<<blocks(pl.n), 256, 0, s>>>(fs + b * pl.n, pl.bk.perm.as<int>(), (long long)pl.n,
-                                                 f + b * pl.n);
+        k_unpermute<<<blocks((pl.n + 3) / 4), 256, 0, s>>>(fs + b * pl.n, pl.bk.invperm.as<int>(), (long long)pl.n,
+                                                           f + b * pl.n);
         NB_LAUNCH();
     }
 }

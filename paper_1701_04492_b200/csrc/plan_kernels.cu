@@ -116,6 +116,11 @@ __global__ void k_bucket_offsets(const Key* __restrict__ keys, long long n, int 
     for (long long b = prev + 1; b <= cur; ++b) off[b] = (int)i;
 }
 
+__global__ void k_invert_perm(const int* __restrict__ perm, long long n, int* __restrict__ inv) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) inv[perm[i]] = (int)i;
+}
+
 __global__ void k_gather_x(const double* __restrict__ x, const int* __restrict__ perm, long long n,
                            double* __restrict__ xs) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -326,6 +331,9 @@ void build_buckets(CorePlan& p, cudaStream_t s) {
     p.bk.rowoff_host.resize(n1 + 1);  // row ranges -> sample ranges on the host (multi-GPU chunking)
     NB_CUDA(cudaMemcpyAsync(p.bk.rowoff_host.data(), p.bk.rowoff.as<int>(), 4 * (n1 + 1),
                             cudaMemcpyDeviceToHost, s));
+    p.bk.invperm.alloc(4 * n);
+    k_invert_perm<<<blocks(n), 256, 0, s>>>(p.bk.perm.as<int>(), (long long)n, p.bk.invperm.as<int>());
+    NB_LAUNCH();
     p.bk.xs.alloc(8 * n);
     k_gather_x<<<blocks(n), 256, 0, s>>>(p.ax.x.as<double>(), p.bk.perm.as<int>(), (long long)n,
                                          p.bk.xs.as<double>());

@@ -38,6 +38,7 @@ struct Axis {
 struct Buckets {
     int log_n1 = 0, log_n2 = 0;  // N = N1*N2
     DevArray xs, perm, rowoff;   // see header comment
+    DevArray invperm;            // invperm[perm[i]] = i: sample j -> its bucket-order slot
     DevArray ds, skey;           // fused transpose core (type I / adjoint / III inner)
     DevArray sort_perm;          // generic transpose core: samples sorted by t (int32)
     DevArray bin_off;            // generic transpose core: N+1 offsets (int32)
@@ -116,7 +117,7 @@ void exec_type2_pass1(const CorePlan& p, const double2* c, double2* Y, size_t r0
                       cudaStream_t s);
 void exec_type2_pass2_rows(const CorePlan& p, const double2* Y, double2* f, size_t r0, size_t r1,
                            long long row0, long long row1, bool sorted_out, cudaStream_t s);
-// f[perm[i]] = fs[i] (bucket order -> natural order), batch vectors of N
+// f[j] = fs[invperm[j]] (bucket order -> natural order; coalesced f writes), batch vectors of N
 void unpermute(const CorePlan& p, const double2* fs, double2* f, size_t batch, cudaStream_t s);
 // F2~^T g = sum_r v_r .* F scatter_t(u_r .* g)   (transforms.hpp:206-221)
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
