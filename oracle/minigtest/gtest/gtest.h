@@ -3,9 +3,11 @@
 // GoogleTest is absent here.  The reference's unit suites
 // (proj/tests/{fft,special,lowrank,oracle,transforms,transform2d}_test.cpp)
 // use only TEST, EXPECT_/ASSERT_ {EQ,NE,LT,LE,GT,GE,NEAR,DOUBLE_EQ,TRUE,FALSE,
-// THROW,NO_THROW} and streamed messages; this header implements exactly that
-// surface so those files compile UNMODIFIED, both against the reference
-// headers (oracle validation) and against include/nufft (drop-in conformance).
+// THROW,NO_THROW} and streamed messages, and cli_test.cpp adds TEST_F fixtures
+// (SetUp/TearDown) and UnitTest::current_test_info()->name(); this header
+// implements exactly that surface so those files compile UNMODIFIED, both
+// against the reference headers (oracle validation) and against include/nufft
+// (drop-in conformance).
 #pragma once
 
 #include <cmath>
@@ -14,11 +16,15 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <iomanip>
 #include <iostream>
 #include <sstream>
 #include <string>
 #include <type_traits>
 #include <vector>
+
+#include <sys/wait.h>
+#include <unistd.h>
 
 namespace minigtest {
 
@@ -34,6 +40,10 @@ inline std::vector<TestInfo>& registry() {
 inline bool& current_failed() {
     static bool f = false;
     return f;
+}
+inline const char*& current_name() {
+    static const char* n = "";
+    return n;
 }
 struct Registrar {
     Registrar(const char* s, const char* n, void (*f)()) { registry().push_back({s, n, f}); }
@@ -99,6 +109,7 @@ inline int run_all() {
     int failed = 0;
     for (const auto& t : registry()) {
         current_failed() = false;
+        current_name() = t.name;
         try {
             t.fn();
         } catch (const std::exception& e) {
@@ -191,5 +202,42 @@ inline int run_all() {
 #define ASSERT_NO_THROW(stmt) EXPECT_NO_THROW(stmt)
 
 namespace testing {
-using Test = struct {};
-}
+class Test {
+  public:
+    virtual ~Test() = default;
+    virtual void SetUp() {}
+    virtual void TearDown() {}
+};
+struct TestInfo {
+    const char* name() const { return ::minigtest::current_name(); }
+};
+class UnitTest {
+  public:
+    static UnitTest* GetInstance() {
+        static UnitTest u;
+        return &u;
+    }
+    const TestInfo* current_test_info() const {
+        static TestInfo info;
+        return &info;
+    }
+};
+}  // namespace testing
+
+#define TEST_F(fixture, name)                                                                        \
+    class MGT_CAT(fixture##_##name, _MgtTest) : public fixture {                                    \
+      public:                                                                                        \
+        void Body();                                                                                 \
+        void Run() {                                                                                 \
+            this->SetUp();                                                                           \
+            Body();                                                                                  \
+            this->TearDown();                                                                        \
+        }                                                                                            \
+    };                                                                                               \
+    static void MGT_CAT(mgt_runf_##fixture##_, name)() {                                             \
+        MGT_CAT(fixture##_##name, _MgtTest) t;                                                       \
+        t.Run();                                                                                     \
+    }                                                                                                \
+    static ::minigtest::Registrar MGT_CAT(mgt_regf_##fixture##_, name)(#fixture, #name,             \
+                                                                       &MGT_CAT(mgt_runf_##fixture##_, name)); \
+    void MGT_CAT(fixture##_##name, _MgtTest)::Body()

@@ -75,16 +75,21 @@ CPP_DIR = os.path.join(HERE, "..", "tests", "cpp")
 # C++ programs written against the drop-in headers (include/nufft) and linked with
 # the library: the usage example / self-check, and the end-to-end timing of
 # exec_nufft2(plan, std::vector) that bench.py reports as e2e.dropin_pageable
-CPP_PROGRAMS = ("example_dropin", "bench_dropin")
+CPP_PROGRAMS = {"example_dropin": os.path.join(CPP_DIR, "example_dropin.cpp"),
+                "bench_dropin": os.path.join(CPP_DIR, "bench_dropin.cpp"),
+                # the reference CLI's subcommands / CSV files / exit codes on the GPU
+                "nufft": os.path.join(HERE, "tools", "nufft_cli.cpp")}
+CLI_BIN = os.path.join(OBJ, "nufft")
 EXAMPLE_BIN = os.path.join(OBJ, "example_dropin")
 BENCH_DROPIN_BIN = os.path.join(OBJ, "bench_dropin")
 
 
 def _build_example() -> None:
-    for name in CPP_PROGRAMS:
-        src = os.path.join(CPP_DIR, name + ".cpp")
+    for name, src in CPP_PROGRAMS.items():
         exe = os.path.join(OBJ, name)
-        if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(LIB), os.path.getmtime(src)):
+        hdrs = [os.path.join(HERE, "..", "include", "nufft", h) for h in os.listdir(os.path.join(HERE, "..", "include", "nufft"))]
+        if os.path.exists(exe) and os.path.getmtime(exe) >= max([os.path.getmtime(LIB), os.path.getmtime(src)] +
+                                                                [os.path.getmtime(h) for h in hdrs]):
             continue
         r = subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(HERE, "..", "include"),
                             src, "-o", exe, "-L" + HERE, "-lnufft_b200",

@@ -80,10 +80,9 @@ template <class Op>
 void host_roundtrip(const double* in, size_t in_doubles, double* out, size_t out_doubles,
                     cudaStream_t s, Op op) {
     nb::DevBuf din(8 * in_doubles, s), dout(8 * out_doubles, s);
-    NB_CUDA(cudaMemcpyAsync(din.get(), in, 8 * in_doubles, cudaMemcpyHostToDevice, s));
+    nb::h2d(din.get(), in, 8 * in_doubles, s);
     op(din.as<double2>(), dout.as<double2>());
-    NB_CUDA(cudaMemcpyAsync(out, dout.get(), 8 * out_doubles, cudaMemcpyDeviceToHost, s));
-    NB_CUDA(cudaStreamSynchronize(s));
+    nb::d2h(out, dout.get(), 8 * out_doubles, s);
 }
 
 void materialize_u(const nb::CorePlan& p, double2* u_dev, cudaStream_t s) {
@@ -458,9 +457,9 @@ int nufft_plan2_exec(const nufft_plan2* plan, const double* c_dev, double* f_dev
 // host->device copy of c_{b+1} and the device->host copy of f_{b-1} overlap the
 // transform of vector b (the PCIe copies of one 2^24 vector take longer than its
 // transform).  Results are identical to the one-shot path (same kernels per vector).
-// The overlap needs page-locked host buffers: with pageable memory the driver
-// stages every copy and the D2H blocks the host, so the batch then runs
-// copy / transform / copy in sequence (same results).
+// Page-locked host buffers only: pageable batches go vector by vector through
+// host_roundtrip, whose staged copies (host_stage.cu) pipeline the chunks of
+// each vector instead.
 namespace {
 struct PipeStreams {  // streams + events, drained before anything they touch is freed
     cudaStream_t st[3] = {};
@@ -524,7 +523,7 @@ int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, 
         const nb::CorePlan& p = plan->core;
         if (len != p.n) nb::throw_invalid("exec_nufft2: length mismatch");
         NB_CUDA(cudaSetDevice(p.device));
-        if (batch > 1) {
+        if (batch > 1 && !nb::host_pageable(c) && !nb::host_pageable(f)) {
             plan2_host_pipelined(p, c, f, batch);
             return;
         }

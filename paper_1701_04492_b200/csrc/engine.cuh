@@ -70,6 +70,14 @@ class DevArray {
     size_t bytes_ = 0;
 };
 
+// host <-> device copies that stage pageable host memory through the library's
+// page-locked ring (host_stage.cu); page-locked memory goes straight to the copy
+// engine.  h2d is ordered on s (returns once `src` may be reused); d2h returns
+// when `dst` holds the data.
+bool host_pageable(const void* p);
+void h2d(void* dst_dev, const void* src_host, size_t bytes, cudaStream_t s);
+void d2h(void* dst_host, const void* src_dev, size_t bytes, cudaStream_t s);
+
 // release the scratch cached in the device's private pool (plan destruction)
 void trim_scratch(int device);
 

@@ -33,19 +33,28 @@ def peak():
         return 6650.0
 
 
+_CLOCKS = {}
+
+
 def timeit(fn, steps, warmup, stream):
+    """CUDA-event ms per call; nvidia-smi clocks sampled over the timed loop (bench.py's
+    ClockSampler) are kept for the record emitted next."""
     import torch
+
+    from bench import ClockSampler
     with torch.cuda.stream(stream):
         for _ in range(warmup):
             fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(steps):
-            fn()
-        e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+    _CLOCKS["last"] = clk.summary()
     return e0.elapsed_time(e1) / steps
 
 
@@ -81,7 +90,7 @@ def main():
         rec = {"config": name, "workload": desc, "points": n_pts, "ms_per_exec": ms,
                "points_per_s": n_pts / (ms / 1e3), "rank_terms": K, "plan_seconds": plan_s,
                "algorithmic_bytes": bytes_alg, "achieved_gbs": gbs,
-               "hbm_frac": (gbs / P) if gbs else None, "peak_gbs": P}
+               "hbm_frac": (gbs / P) if gbs else None, "peak_gbs": P, "clocks": _CLOCKS.get("last")}
         if extra:
             rec.update(extra)
         print(json.dumps(rec), flush=True)
@@ -188,23 +197,29 @@ def main():
         torch.cuda.empty_cache()
 
     if "cfg4" in want:
-        rng = np.random.default_rng(74)
+        # both B families: seed 4041 draws no sample on the node at 1 (bTrivial), seed 4040
+        # draws one (B non-trivial: the beta family runs as K dot products); the reference's
+        # own inputs (GaussianSampler, tests/fullsize_ref.py).  Algorithmic bytes count the
+        # K x K_inner terms both cases actually need (32 + 12 + 32 K K_inner per point).
         n = 1 << 22
-        x = rng.random(n)
-        w = rng.uniform(0, n, n)
-        t0 = time.perf_counter()
-        p = nb.plan_nufft3(x, w, 1e-9)
-        torch.cuda.synchronize()
-        ps = time.perf_counter() - t0
-        terms = p.effective_rank() * p.rank_inner
-        c = torch.randn(n, dtype=torch.complex128, device="cuda")
-        f = torch.empty_like(c)
-        ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), max(2, args.steps // 3),
-                    1, stream)
-        emit("cfg4", "NUFFT-III N=2^22 eps=1e-9 x U[0,1), omega U[0,N)", n, ms, (32 + 12 + 32 * terms) * n,
-             terms, ps, {"bTrivial": p.bTrivial, "effective_rank": p.effective_rank(), "rank_inner": p.rank_inner})
-        del p, c, f
-        torch.cuda.empty_cache()
+        for seed, tag in ((4041, "cfg4t"), (4040, "cfg4n")):
+            smp = nb.GaussianSampler(seed)
+            x = smp.uniform_vector(n, 0.0, 1.0)
+            w = smp.uniform_vector(n, 0.0, float(n))
+            c = dev(smp.complex_vector(n))
+            t0 = time.perf_counter()
+            p = nb.plan_nufft3(x, w, 1e-9)
+            torch.cuda.synchronize()
+            ps = time.perf_counter() - t0
+            terms = p.rank_a * p.rank_inner
+            f = torch.empty_like(c)
+            ms = timeit(lambda: p.execute_device(c.data_ptr(), f.data_ptr(), 1, sh), max(2, args.steps // 2),
+                        1, stream)
+            emit(tag, "NUFFT-III N=2^22 eps=1e-9 x U[0,1), omega U[0,N)", n, ms, (32 + 12 + 32 * terms) * n,
+                 terms, ps, {"bTrivial": p.bTrivial, "effective_rank": p.effective_rank(),
+                             "rank_inner": p.rank_inner})
+            del p, c, f
+            torch.cuda.empty_cache()
 
     if "cfg5" in want:
         rng = np.random.default_rng(75)

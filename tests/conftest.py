@@ -27,7 +27,8 @@ def pytest_collection_modifyitems(session, config, items):
     """Start the reference's own full-size runs (tests/fullsize_ref.py) as soon
     as test_gpu_fullsize.py is part of the selected session, so the CPU work
     overlaps the GPU tests that run before it."""
-    if not any("test_gpu_fullsize" in it.nodeid for it in items):
+    sel = [it.nodeid for it in items if "test_gpu_fullsize" in it.nodeid]
+    if not sel:
         return
     from oracle import pyoracle
     if not pyoracle.available("reference"):
@@ -36,7 +37,8 @@ def pytest_collection_modifyitems(session, config, items):
 
     import fullsize_ref
     d = tempfile.mkdtemp(prefix="nufft_fullsize_ref_")
-    _FULLSIZE["runner"] = fullsize_ref.Runner(d)
+    need = fullsize_ref.runs_for(sel)
+    _FULLSIZE["runner"] = fullsize_ref.Runner(d, runs=need)
 
 
 def pytest_sessionfinish(session, exitstatus):

@@ -138,12 +138,20 @@ if __name__ == "__main__":
     run_reference(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 1)
 
 
+def runs_for(nodeids) -> tuple:
+    """Which reference runs the selected test_gpu_fullsize items need."""
+    tags = {"cfg2": ("cfg2_",), "cfg3": ("cfg3_",), "cfg4t": ("cfg4t",), "cfg4n": ("cfg4n",),
+            "cfg5": ("cfg5_",)}
+    need = tuple(r for r in RUNS if any(any(t in nid for t in tags[r]) for nid in nodeids))
+    return need or RUNS
+
+
 class Runner:
     """Background reference processes, one per entry of RUNS, started at test
     collection (tests/conftest.py) so they run on the host cores while the
     other GPU tests proceed."""
 
-    def __init__(self, outdir: str, threads: int | None = None):
+    def __init__(self, outdir: str, threads: int | None = None, runs=RUNS):
         import subprocess
         self.outdir = outdir
         cores = os.cpu_count() or 4
@@ -151,7 +159,7 @@ class Runner:
         # other four are single-threaded in the reference
         t2 = threads or max(1, cores - 8)  # leave cores for pytest itself
         self.procs = {}
-        for cfg in RUNS:
+        for cfg in runs:
             log = open(os.path.join(outdir, f"{cfg}.log"), "w")
             self.procs[cfg] = subprocess.Popen(
                 [sys.executable, os.path.abspath(__file__), cfg, outdir, str(t2 if cfg == "cfg2" else 1)],
@@ -160,6 +168,8 @@ class Runner:
     def result(self, cfg: str, timeout: float = 1500.0):
         """(output, info) of one config; waits for its process."""
         run = "cfg2" if cfg == "cfg2b8" else cfg
+        if run not in self.procs:
+            raise RuntimeError(f"reference run {run} was not started for this session")
         path = os.path.join(self.outdir, f"{cfg}.npy")
         t0 = time.time()
         while not os.path.exists(path):

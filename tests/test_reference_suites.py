@@ -5,7 +5,8 @@
   the same two red cells) — the oracle build is pinned by the reference's own
   known answers and tolerances.
 * GPU: conf_<suite> = the same sources against the drop-in headers in
-  include/nufft linked to libnufft_b200.so — the conformance suite.
+  include/nufft linked to libnufft_b200.so — the conformance suite; conf_cli
+  runs the reference's CLI tests against the B200 CLI binary.
 """
 from __future__ import annotations
 
@@ -46,8 +47,11 @@ def test_reference_acceptance_reproduces_recorded_output():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", SUITES)
+@pytest.mark.parametrize("suite", SUITES + ["cli"])
 def test_reference_unit_suite_on_b200_dropin(nb, suite):
+    """conf_cli is the reference CLI's own test (proj/tests/cli_test.cpp: CSV round
+    trips, exit codes 0/1/2/3, transform/verify/bench/cgstudy end to end) against
+    the drop-in csv/oracle/random headers and the B200 CLI (tools/nufft_cli.cpp)."""
     r = subprocess.run([_bin(f"conf_{suite}")], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
 
