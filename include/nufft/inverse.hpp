@@ -87,17 +87,14 @@ struct CgReport {
 
 namespace detail {
 
-inline double norm2(const ComplexVector& v) {
-    double s = 0.0;
-    for (const auto& z : v) s += std::norm(z);
-    return std::sqrt(s);
+/// Re <a, b> = sum_j Re(conj(a_j) b_j), summed in index order
+inline double dot_real(const ComplexVector& a, const ComplexVector& b) {
+    double acc = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) acc += a[i].real() * b[i].real() + a[i].imag() * b[i].imag();
+    return acc;
 }
 
-inline double dot_real(const ComplexVector& a, const ComplexVector& b) {
-    double s = 0.0;
-    for (std::size_t j = 0; j < a.size(); ++j) s += a[j].real() * b[j].real() + a[j].imag() * b[j].imag();
-    return s;
-}
+inline double norm2(const ComplexVector& v) { return std::sqrt(dot_real(v, v)); }
 
 inline std::size_t default_cg_max_iter(std::size_t n) { return nufft_default_cg_max_iter(n); }
 
@@ -114,45 +111,51 @@ inline CgReport cg_report(const nufft_cg_report& r, ComplexVector solution, std:
 
 }  // namespace detail
 
-/// Plain CG for a Hermitian positive (semi)definite host operator
-/// (inverse.hpp:118-157; same recurrences, same stopping rule).
+/// Conjugate gradients on the host for a Hermitian positive (semi)definite
+/// operator given as a callable (the reference's cg_solve, inverse.hpp:118-157):
+/// x0 = 0, the real part of <p, A p> as the step denominator (a non-positive one
+/// ends the iteration), relative residual |r_k| / |rhs| recorded after every
+/// step and compared with tol, at most max_iter steps.  The device solvers
+/// below (inufft1 / inufft2) run the same iteration on the GPU.
 template <typename Operator>
 CgReport cg_solve(Operator&& apply, const ComplexVector& rhs, double tol, std::size_t max_iter) {
     if (!(tol > 0.0)) throw std::domain_error("cg_solve: tol must be positive");
-    const std::size_t n = rhs.size();
-    CgReport report;
-    report.solution.assign(n, Complex(0, 0));
-    const double rhs_norm = detail::norm2(rhs);
-    if (rhs_norm == 0.0) {
-        report.converged = true;
-        return report;
+    CgReport out;
+    ComplexVector& x = out.solution;
+    x.assign(rhs.size(), Complex(0.0, 0.0));
+    const double scale = detail::norm2(rhs);
+    if (scale == 0.0) {  // A x = 0 is solved by x = 0
+        out.converged = true;
+        return out;
     }
-    ComplexVector r = rhs;
-    ComplexVector p = r;
-    double rho = detail::dot_real(r, r);
-    for (std::size_t it = 1; it <= max_iter; ++it) {
-        const ComplexVector ap = apply(p);
-        const double denom = detail::dot_real(p, ap);
-        if (denom <= 0.0) break;
-        const double alpha = rho / denom;
-        for (std::size_t j = 0; j < n; ++j) {
-            report.solution[j] += alpha * p[j];
-            r[j] -= alpha * ap[j];
+    ComplexVector resid(rhs), dir(rhs);
+    double rr = detail::dot_real(resid, resid);
+    auto update = [](ComplexVector& y, double a, const ComplexVector& v) {
+        for (std::size_t i = 0; i < y.size(); ++i) y[i] += a * v[i];
+    };
+    std::size_t k = 0;
+    while (k < max_iter) {
+        const ComplexVector q = apply(dir);
+        const double curv = detail::dot_real(dir, q);
+        if (!(curv > 0.0)) break;  // lost positive definiteness (or a zero direction)
+        const double step = rr / curv;
+        update(x, step, dir);
+        update(resid, -step, q);
+        const double rr_new = detail::dot_real(resid, resid);
+        ++k;
+        out.iterations = k;
+        out.relativeResidual = std::sqrt(rr_new) / scale;
+        out.residualHistory.push_back(out.relativeResidual);
+        if (out.relativeResidual <= tol) {
+            out.converged = true;
+            return out;
         }
-        const double rho_next = detail::dot_real(r, r);
-        report.iterations = it;
-        report.relativeResidual = std::sqrt(rho_next) / rhs_norm;
-        report.residualHistory.push_back(report.relativeResidual);
-        if (report.relativeResidual <= tol) {
-            report.converged = true;
-            return report;
-        }
-        const double beta = rho_next / rho;
-        for (std::size_t j = 0; j < n; ++j) p[j] = r[j] + beta * p[j];
-        rho = rho_next;
+        const double ratio = rr_new / rr;
+        for (std::size_t i = 0; i < dir.size(); ++i) dir[i] = resid[i] + ratio * dir[i];
+        rr = rr_new;
     }
-    report.relativeResidual = std::sqrt(rho) / rhs_norm;
-    return report;
+    out.relativeResidual = std::sqrt(rr) / scale;
+    return out;
 }
 
 /// Inverse type II on the device (inverse.hpp:171-183).

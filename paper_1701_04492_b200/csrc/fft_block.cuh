@@ -363,11 +363,18 @@ __device__ __forceinline__ int fft2l_slot(int tid, int b) {
     return g * 256 + 16 * u + (b ^ fft2l_swz(g) ^ (u & 7));
 }
 
-template <int SIGN, class Bar>
+// PreWrite: called once, after the first-level DFT and twiddles and before the
+// first write to buf — the point by which buf must be free (callers whose
+// buf is still being read by the TMA engine wait there, not before the FFT).
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+template <int SIGN, class Bar, class PreWrite = NoHook>
 __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
-                                             Bar bar) {
+                                             Bar bar, PreWrite pre_write = PreWrite()) {
     dft<16, SIGN>(v);
     apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
+    pre_write();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 256 + (tid ^ fft2l_swz(k1))] = v[k1];
     bar();

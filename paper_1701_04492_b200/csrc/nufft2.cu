@@ -377,9 +377,13 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 if (r > 0) tm_st16(tc_s + 16 * j, sv);
             }
-            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // engine done with buf
-            gsync();  // previous term's reads of buf (exchange, TMA) are done
-            block_fft_2l<-1>(v, buf, tid, T, gsync);
+            // buf must be free (the engine has read the previous term's box) only when the
+            // exchange first writes it: wait there, after the first-level DFT, so the TMA
+            // drain of the previous column-term overlaps that compute
+            block_fft_2l<-1>(v, buf, tid, T, gsync, [&] {
+                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                gsync();
+            });
             gsync();  // exchange reads done: buf becomes the staging box
 #pragma unroll
             for (int b = 0; b < 16; ++b) stg[256 * b] = cmul(v[b], cmul(base, step[b]));
@@ -1255,6 +1259,7 @@ __global__ void __launch_bounds__(512, 1)
         const bool has_next = row < n1;
         const int last = nt - 1;
         const int lastgrp = (S0 + last) & 1;  // group of the unit's last update
+        bool pre_loaded = false;              // v holds the next unit's first row
         for (int i = (grp - S0) & 1; i < nt; i += 2) {
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
@@ -1262,14 +1267,26 @@ __global__ void __launch_bounds__(512, 1)
                 if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
             }
-            // this group's next row (step i + 2) is in flight during the update; a later
-            // one (step i + 2 kFsL2Prefetch) is warmed in L2
+            // this group's next row (step i + 2) is in flight during the update — across the
+            // unit boundary too: the group that transforms the next unit's first row at the
+            // boundary loads it during its last update of this unit; a later row (step
+            // i + 2 kFsL2Prefetch, continuing into the next unit) is warmed in L2
             have = i + 2 < nt;
-            if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
-            if (tid == 0 && i + 2 * kFsL2Prefetch < nt && (urow & 1) == 0) {
-                const void* nxt = Y + y_index(rr - 2 * kFsL2Prefetch, N, p.log_n2, urow, 0);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
-                             "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
+            if (have) {
+                fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
+            } else if (has_next && grp != lastgrp) {
+                fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
+                pre_loaded = true;
+            }
+            if (tid == 0) {
+                const int ia = i + 2 * kFsL2Prefetch;  // step to warm (>= nt: the next unit's)
+                const long long prow = ia < nt ? urow : row;
+                const int prr = ia < nt ? rr - 2 * kFsL2Prefetch : last - (ia - nt);
+                if ((ia < nt || (has_next && ia - nt < nt)) && (prow & 1) == 0) {
+                    const void* nxt = Y + y_index(prr, N, p.log_n2, prow, 0);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                                 "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
+                }
             }
             if (i > 0) {  // the other group's update of step i-1 is done
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
@@ -1322,7 +1339,7 @@ __global__ void __launch_bounds__(512, 1)
         pre = false;
         if (grp != lastgrp) {
             if (has_next) {
-                fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
+                if (!pre_loaded) fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
                 pre = true;
             }
