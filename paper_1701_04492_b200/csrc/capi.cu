@@ -922,6 +922,7 @@ int nufft_plan3_create(const double* x_raw, const double* omega, size_t n_x, siz
         NB_CUDA(cudaStreamSynchronize(s));
         st.btrivial = wrap == 0;
         st.kc = st.btrivial ? st.a.K : 2 * st.a.K;
+        nb::build_type3_order(st, s);
         // inner type-I plan on omega (transforms.hpp:378)
         nb::finish_core(st.inner, st.inner.ax.gamma_raw, s);
         if (!st.inner.fused) nb::build_bins(st.inner, s);

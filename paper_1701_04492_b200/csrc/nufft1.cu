@@ -129,23 +129,27 @@ __global__ void k3_beta_dot_final(const double2* __restrict__ part, int r0, int 
 
 // f[j] = sum_r u^A_r(delta_j) Z_r,j with Z_r,j = y_r[t_j] (beta_j = 0) or D_r
 // (beta_j = 1) — both families and the K per-term accumulations of the
-// reference's exec_nufft3 (transforms.hpp:386-392) in one sample-ordered pass.
+// reference's exec_nufft3 (transforms.hpp:386-392) in one pass over the samples
+// in ascending t (plan order, Plan3State::ord_*), so consecutive threads read
+// neighbouring y_r[t] and only f[j] is scattered.
 // u_r = 2 exp(2ih) (ih)^r g_r(h^2): Horner in r over acc <- acc (ih) + g_r Z_r,
 // g_r by the backward Bessel recurrence g_{r-1} = r g_r - w g_{r+1} from two
 // series values (as in the type-II pass 2, nufft2.cu).
 __global__ void k3_epilogue(const double2* __restrict__ Y, const double2* __restrict__ D,
-                            const double* __restrict__ delta, const long long* __restrict__ sv,
-                            const long long* __restrict__ tv, long long n, int K, int deg_top0, int deg_top1,
+                            const int* __restrict__ ord_perm, const unsigned* __restrict__ ord_key,
+                            const double* __restrict__ ord_delta, long long n, int K, int deg_top0, int deg_top1,
                             int uniform, double2* __restrict__ f) {
-    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const long long t = tv[j];
-    const bool beta = sv[j] != t;  // s = N, t = 0: the node at 1 (transforms.hpp:345-350)
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned key = ord_key[i];
+    const long long t = key & 0x7fffffffu;
+    const bool beta = (key >> 31) != 0;  // s = N, t = 0: the node at 1 (transforms.hpp:345-350)
+    const int j = ord_perm[i];
     if (uniform) {
         f[j] = beta ? D[0] : Y[t];
         return;
     }
-    const double h = half_phase(delta[j]);
+    const double h = half_phase(ord_delta[i]);
     const double w = h * h;
     double g1 = bessel_g_rt(K, deg_top1, w);      // g_K
     double g0 = bessel_g_rt(K - 1, deg_top0, w);  // g_{K-1}
@@ -161,7 +165,7 @@ __global__ void k3_epilogue(const double2* __restrict__ Y, const double2* __rest
     }
     double sn, cs;
     sincos(2.0 * h, &sn, &cs);
-    f[j] = cmul(make_double2(2.0 * cs, 2.0 * sn), acc);
+    __stcs(f + j, cmul(make_double2(2.0 * cs, 2.0 * sn), acc));
 }
 
 }  // namespace
@@ -225,8 +229,8 @@ void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch,
         } else {
             NB_CUDA(cudaMemsetAsync(D.get(), 0, sizeof(double2) * K, s));
         }
-        k3_epilogue<<<blocks(N), 256, 0, s>>>(Y.as<double2>(), D.as<double2>(), p.a.ax.delta.as<double>(),
-                                              p.a.ax.s.as<long long>(), p.a.ax.t.as<long long>(), (long long)N,
+        k3_epilogue<<<blocks(N), 256, 0, s>>>(Y.as<double2>(), D.as<double2>(), p.ord_perm.as<int>(),
+                                              p.ord_key.as<unsigned>(), p.ord_delta.as<double>(), (long long)N,
                                               (int)K, deg0, deg1, uni, f + b * N);
         NB_LAUNCH();
     }

@@ -30,6 +30,7 @@
 #include "bessel.cuh"
 #include "fft_block.cuh"
 #include "plans.hpp"
+#include "tmem.cuh"
 
 namespace nb {
 
@@ -256,6 +257,241 @@ __global__ void __launch_bounds__(LM / 16, 1)
     }
 }
 
+// ---------------------------------------------------------------- column stage, m = 4096
+// Two FFT groups of 256 threads alternate the Kx*Ky column steps of a unit
+// (column tx, <= 4608 samples), the organization of the type-II fused pass 2
+// (k2_pass2_fs, nufft2.cu) with one more loop level:
+//   per r1 (outer, Kx-1 .. 0): the R_r1 column is staged in shared memory once;
+//     per r2 (Ky-1 .. 0), group (step % 2): v = vy_r2 .* column, two-level FFT,
+//     X left in place in the group's buffer; then, after the other group's
+//     update of the previous step (named-barrier hand-off), every sample of the
+//     unit: S <- S (i hy) + gy_r2 X[ty], gy_{r2-1} = r2 gy_r2 - hy^2 gy_{r2+1}
+//     (backward Bessel recurrence) — state (S, gy pair, hy, slot, hx) in TMEM;
+//   block end: A <- A (i hx) + gx_r1(hx^2) S with A in a sorted-order HBM
+//     scratch (coalesced), and for r1 = 0 f[perm] = 4 exp(2i(hx + hy)) A.
+// The FFT of one group overlaps the sample update of the other; each step
+// moves no HBM bytes except the L2-resident vy row.
+struct Col2Shape {
+    static constexpr int G = 256;
+    static constexpr int SLOTS = 18;  // CAP = 4608 = 1.125 x 4096 samples per unit
+    static constexpr int CAP = SLOTS * G;
+    static constexpr int CH = 2;
+    static constexpr int COL_S = 0, COL_G = 4 * SLOTS, COL_HY = 8 * SLOTS, COL_T = 10 * SLOTS,
+                         COL_HX = 11 * SLOTS, COLS = 13 * SLOTS;
+    static constexpr size_t SMEM = sizeof(double2) * (3 * kBuf2l + FftShapeX<4096>::TW_LEN);
+    static_assert(COLS <= 256 && SLOTS % CH == 0, "TMEM layout");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+struct Col2Params {
+    long long m, n;
+    int kx, ky;
+    int ux_uniform, uy_uniform;
+    const double* dxs;
+    const double* dys;
+    const unsigned short* tys;
+    const int* perm;
+    const int* coloff;
+    const double* vyt;  // ky x m
+    double2* A;         // sorted-order scratch
+    int degx[kRankCap];
+    int degy_top0, degy_top1;  // relative-accuracy degrees of gy_{Ky-1}, gy_{Ky}
+};
+
+__device__ __forceinline__ void c2_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void c2_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(512, 1)
+    k2d_cols_fs(const double2* __restrict__ R, double2* __restrict__ f, Col2Params p) {
+    using W = Col2Shape;
+    constexpr int G = 256, CH = 2;
+    constexpr int BAR_G = 1, BAR_H = 3;  // group barriers 1-2, hand-off 3-4 (by arriving group)
+    constexpr int NCH = W::SLOTS / CH;   // chunks of a unit
+    extern __shared__ double2 smem[];
+    __shared__ unsigned tmem_base;
+    const int grp = threadIdx.x >> 8;
+    const int tid = threadIdx.x & (G - 1);
+    double2* buf = smem + grp * kBuf2l;
+    double2* rcol = smem + 2 * kBuf2l;
+    double2* tw = smem + 3 * kBuf2l;
+    twiddle_table_build<4096>(tw, threadIdx.x, 2 * G);
+    Twiddles<4096> T;
+    twiddle_init<4096>(T, tw, tid);
+    if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    // thread tid of both groups shares the TMEM state of its sample slots
+    const unsigned tl = tm_lane_base(tmem_base) + (unsigned)(((tid >> 7) & 1) * 256);
+    const int gbar = BAR_G + grp;
+    auto gsync = [gbar] { c2_bar_sync(gbar, G); };
+    const long long mn = p.m * p.n;
+    const int nsteps = p.ky;
+    const double sx = p.ux_uniform ? 1.0 : 2.0, sy = p.uy_uniform ? 1.0 : 2.0;
+    int S0 = 0;  // global step index (group of step = index & 1)
+    for (long long tx = blockIdx.x; tx < p.n; tx += gridDim.x) {
+        const int beg = p.coloff[tx], end = p.coloff[tx + 1];
+        for (int cb = beg; cb < end; cb += W::CAP) {
+            const int cnt = min(W::CAP, end - cb);
+            const int nch = ((cnt + G - 1) / G + CH - 1) / CH;  // occupied chunks (CTA-uniform)
+            // unit setup (this group's chunks): hy, hx, gather slot of X[ty]
+            for (int k = grp; k < nch; k += 2) {
+                unsigned hy[2 * CH], hx[2 * CH], sl[CH];
+#pragma unroll
+                for (int u = 0; u < CH; ++u) {
+                    const int i = tid + (CH * k + u) * G;
+                    const bool ok = i < cnt;
+                    const double y = (ok && !p.uy_uniform) ? half_phase(p.dys[cb + i]) : 0.0;
+                    const double x = (ok && !p.ux_uniform) ? half_phase(p.dxs[cb + i]) : 0.0;
+                    hy[2 * u] = lo32(y);
+                    hy[2 * u + 1] = hi32(y);
+                    hx[2 * u] = lo32(x);
+                    hx[2 * u + 1] = hi32(x);
+                    sl[u] = ok ? (unsigned)fft2l_slot_of(p.tys[cb + i]) : 0u;
+                }
+                tm_stn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hy);
+                tm_stn<2 * CH>(tl + W::COL_HX + 2 * CH * k, hx);
+                tm_stn<CH>(tl + W::COL_T + CH * k, sl);
+            }
+            tm_wait_st();
+            for (int r1 = p.kx - 1; r1 >= 0; --r1) {
+                // block start: the R_r1 column (stride n) into shared memory; S = 0 and the
+                // gy pair (gy_{Ky-1}, gy_Ky) by the series, this group's chunks
+                const double2* col = R + (long long)r1 * mn + tx;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    rcol[threadIdx.x + 512 * q] = __ldcg(col + (long long)(threadIdx.x + 512 * q) * p.n);
+                for (int k = grp; k < nch; k += 2) {
+                    unsigned hy[2 * CH], sv[4 * CH], gv[4 * CH];
+                    tm_ldn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hy);
+                    tm_wait_ld();
+                    double w[CH], ga[CH], gb[CH];
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) {
+                        const double h = mk64(hy[2 * u], hy[2 * u + 1]);
+                        w[u] = h * h;
+                    }
+                    series_deg<CH>(ga, w, kBes + (nsteps - 1) * kSeriesTerms, p.degy_top0);
+                    series_deg<CH>(gb, w, kBes + nsteps * kSeriesTerms, p.degy_top1);
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) {
+                        gv[4 * u] = lo32(ga[u]);
+                        gv[4 * u + 1] = hi32(ga[u]);
+                        gv[4 * u + 2] = lo32(gb[u]);
+                        gv[4 * u + 3] = hi32(gb[u]);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) sv[4 * u + c] = 0u;
+                    }
+                    tm_stn<4 * CH>(tl + W::COL_S + 4 * CH * k, sv);
+                    tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+                }
+                tm_wait_st();
+                tm_fence_before();
+                __syncthreads();  // column staged, block state set
+                tm_fence_after();
+                for (int i = (grp - S0) & 1; i < nsteps; i += 2) {
+                    const int r2 = nsteps - 1 - i;
+                    const double* vy = p.vyt + (long long)r2 * p.m;
+                    double2 v[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
+                    gsync();  // this group's gathers from buf (its previous step) are done
+                    block_fft_2l<-1>(v, buf, tid, T, gsync);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
+                    gsync();  // X complete
+                    if (i > 0) {  // the other group's update of step i-1 is done
+                        c2_bar_sync(BAR_H + (grp ^ 1), 2 * G);
+                        tm_fence_after();
+                    }
+                    const double rd = (double)r2;
+#pragma unroll 1
+                    for (int k = 0; k < nch; ++k) {
+                        unsigned sv[4 * CH], gv[4 * CH], hv[2 * CH], t2v[CH];
+                        tm_ldn<4 * CH>(tl + W::COL_S + 4 * CH * k, sv);
+                        tm_ldn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+                        tm_ldn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hv);
+                        tm_ldn<CH>(tl + W::COL_T + CH * k, t2v);
+                        tm_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < CH; ++u) {
+                            const double2 X = buf[t2v[u]];
+                            const double h = mk64(hv[2 * u], hv[2 * u + 1]);
+                            const double gr = mk64(gv[4 * u], gv[4 * u + 1]);
+                            const double gr1 = mk64(gv[4 * u + 2], gv[4 * u + 3]);
+                            const double ax = mk64(sv[4 * u], sv[4 * u + 1]);
+                            const double ay = mk64(sv[4 * u + 2], sv[4 * u + 3]);
+                            const double nx = __fma_rn(gr, X.x, -h * ay);
+                            const double ny = __fma_rn(gr, X.y, h * ax);
+                            const double gm1 = __fma_rn(rd, gr, -(h * h) * gr1);  // gy_{r2-1}
+                            gv[4 * u] = lo32(gm1);
+                            gv[4 * u + 1] = hi32(gm1);
+                            gv[4 * u + 2] = lo32(gr);
+                            gv[4 * u + 3] = hi32(gr);
+                            sv[4 * u] = lo32(nx);
+                            sv[4 * u + 1] = hi32(nx);
+                            sv[4 * u + 2] = lo32(ny);
+                            sv[4 * u + 3] = hi32(ny);
+                        }
+                        tm_stn<4 * CH>(tl + W::COL_S + 4 * CH * k, sv);
+                        tm_stn<4 * CH>(tl + W::COL_G + 4 * CH * k, gv);
+                    }
+                    tm_wait_st();
+                    tm_fence_before();
+                    if (i < nsteps - 1) c2_bar_arrive(BAR_H + grp, 2 * G);  // hand off step i+1
+                }
+                tm_fence_before();
+                __syncthreads();  // every update of the block done; rcol free
+                tm_fence_after();
+                // block end (this group's chunks): A <- A (i hx) + gx_r1(hx^2) S; r1 = 0 writes f
+                const double* ax_c = kBes + r1 * kSeriesTerms;
+                const int dgx = p.degx[r1];
+                for (int k = grp; k < nch; k += 2) {
+                    unsigned sv[4 * CH], hx[2 * CH], hy[2 * CH];
+                    tm_ldn<4 * CH>(tl + W::COL_S + 4 * CH * k, sv);
+                    tm_ldn<2 * CH>(tl + W::COL_HX + 2 * CH * k, hx);
+                    if (r1 == 0) tm_ldn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hy);
+                    tm_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) {
+                        const int i = tid + (CH * k + u) * G;
+                        if (i >= cnt) continue;
+                        const double h = mk64(hx[2 * u], hx[2 * u + 1]);
+                        const double gx = p.ux_uniform ? 1.0 : bessel_g_rt(r1, dgx, h * h);
+                        const double2 S = make_double2(mk64(sv[4 * u], sv[4 * u + 1]), mk64(sv[4 * u + 2], sv[4 * u + 3]));
+                        double2 A = cscale(S, gx);
+                        if (r1 != p.kx - 1) {
+                            const double2 prev = p.A[cb + i];
+                            A.x = __fma_rn(-h, prev.y, A.x);
+                            A.y = __fma_rn(h, prev.x, A.y);
+                        }
+                        if (r1 > 0) {
+                            p.A[cb + i] = A;
+                        } else {
+                            const double hyv = mk64(hy[2 * u], hy[2 * u + 1]);
+                            double sn, cs;
+                            sincos(2.0 * (h + hyv), &sn, &cs);
+                            const double sc = sx * sy;
+                            __stcs(f + p.perm[cb + i], cmul(make_double2(sc * cs, sc * sn), A));
+                        }
+                    }
+                }
+                S0 += nsteps;
+            }
+            tm_fence_before();
+            __syncthreads();  // unit done: slots and rcol free for the next unit
+            tm_fence_after();
+        }
+    }
+    tm_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
+}
+
 __global__ void k2d_keys(const long long* __restrict__ tx, long long count, unsigned* __restrict__ keys,
                          int* __restrict__ idx) {
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -316,8 +552,34 @@ void launch_rows(const double2* C, double2* R, const Plan2DState& st, cudaStream
     NB_LAUNCH();
 }
 
+void launch_cols_fs(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s) {
+    const DeviceCtx& ctx = DeviceCtx::get(st.device);
+    Col2Params p{};
+    p.m = (long long)st.m;
+    p.n = (long long)st.n;
+    p.kx = (int)st.kx;
+    p.ky = (int)st.ky;
+    p.ux_uniform = st.ux_uniform ? 1 : 0;
+    p.uy_uniform = st.uy_uniform ? 1 : 0;
+    p.dxs = st.fz.dxs.as<double>();
+    p.dys = st.fz.dys.as<double>();
+    p.tys = st.fz.tys.as<unsigned short>();
+    p.perm = st.fz.perm.as<int>();
+    p.coloff = st.fz.coloff.as<int>();
+    p.vyt = st.fz.vyt.as<double>();
+    p.A = A;
+    for (size_t r = 0; r < st.deg_x.size() && r < (size_t)kRankCap; ++r) p.degx[r] = st.deg_x[r];
+    p.degy_top0 = bessel_series_degree_rel(st.uy_uniform ? 0.0 : st.ay.gamma, (int)st.ky - 1);
+    p.degy_top1 = bessel_series_degree_rel(st.uy_uniform ? 0.0 : st.ay.gamma, (int)st.ky);
+    set_smem(k2d_cols_fs, Col2Shape::SMEM);
+    const int grid = (int)std::min<long long>((long long)st.n, (long long)ctx.sms);
+    k2d_cols_fs<<<grid, 512, Col2Shape::SMEM, s>>>(R, f, p);
+    NB_LAUNCH();
+}
+
 template <int LM>
 void launch_cols(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s) {
+    if constexpr (LM == 4096) return launch_cols_fs(R, f, A, st, s);
     const DeviceCtx& ctx = DeviceCtx::get(st.device);
     constexpr size_t SM = ColShape<LM>::SMEM;
     ColParams p{};

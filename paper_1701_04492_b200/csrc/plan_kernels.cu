@@ -116,6 +116,25 @@ __global__ void k_bucket_offsets(const Key* __restrict__ keys, long long n, int 
     for (long long b = prev + 1; b <= cur; ++b) off[b] = (int)i;
 }
 
+// key t_j (< 2^31) and the wraparound flag beta_j = (s_j != t_j) in bit 31
+__global__ void k_t3_keys(const long long* __restrict__ sv, const long long* __restrict__ tv, long long n,
+                          unsigned* __restrict__ keys, unsigned* __restrict__ flags, int* __restrict__ idx) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    keys[j] = (unsigned)tv[j];
+    flags[j] = (unsigned)tv[j] | (sv[j] != tv[j] ? 0x80000000u : 0u);
+    idx[j] = (int)j;
+}
+__global__ void k_t3_gather(const int* __restrict__ perm, const unsigned* __restrict__ flags,
+                            const double* __restrict__ delta, long long n, unsigned* __restrict__ key,
+                            double* __restrict__ ds) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int j = perm[i];
+    key[i] = flags[j];
+    ds[i] = delta[j];
+}
+
 __global__ void k_invert_perm(const int* __restrict__ perm, long long n, int* __restrict__ inv) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) inv[perm[i]] = (int)i;
@@ -405,4 +424,27 @@ void cheb_eval(const double* pts_dev, size_t n, size_t K, double* out_dev, cudaS
     if (h) throw_domain("cheb_eval_matrix: point outside [-1, 1]");
 }
 
+}  // namespace nb
+
+namespace nb {
+void build_type3_order(Plan3State& st, cudaStream_t s) {
+    const size_t n = st.a.n;
+    DevBuf keys(4 * n, s), keys_out(4 * n, s), flags(4 * n, s), idx(4 * n, s);
+    st.ord_perm.alloc(4 * n);
+    k_t3_keys<<<blocks(n), 256, 0, s>>>(st.a.ax.s.as<long long>(), st.a.ax.t.as<long long>(), (long long)n,
+                                        keys.as<unsigned>(), flags.as<unsigned>(), idx.as<int>());
+    NB_LAUNCH();
+    const int bits = std::max(1, ilog2(n));
+    size_t temp = 0;
+    NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
+                                            idx.as<int>(), st.ord_perm.as<int>(), (int)n, 0, bits, s));
+    DevBuf tb(temp, s);
+    NB_CUDA(cub::DeviceRadixSort::SortPairs(tb.get(), temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
+                                            idx.as<int>(), st.ord_perm.as<int>(), (int)n, 0, bits, s));
+    st.ord_key.alloc(4 * n);
+    st.ord_delta.alloc(8 * n);
+    k_t3_gather<<<blocks(n), 256, 0, s>>>(st.ord_perm.as<int>(), flags.as<unsigned>(), st.a.ax.delta.as<double>(),
+                                          (long long)n, st.ord_key.as<unsigned>(), st.ord_delta.as<double>());
+    NB_LAUNCH();
+}
 }  // namespace nb

@@ -67,6 +67,9 @@ struct Plan3State {
     DevArray omega;    // raw frequencies (fp64)
     bool btrivial = true;
     size_t kc = 0;
+    // samples in ascending t (stable in j) for the sample-ordered epilogue of
+    // exec_type3: original index, key = t | beta << 31, delta
+    DevArray ord_perm, ord_key, ord_delta;
 };
 
 struct Plan2DState {
@@ -97,6 +100,8 @@ void assign_frequencies(Axis& ax, const double* omega, bool on_device, size_t n,
 void finish_core(CorePlan& p, double gamma_for_factors, cudaStream_t s);
 void build_buckets(CorePlan& p, cudaStream_t s);
 void build_bins(CorePlan& p, cudaStream_t s);
+// Plan3State::ord_* from a's samples (type-III epilogue order)
+void build_type3_order(Plan3State& st, cudaStream_t s);
 
 // materialize the reference-form factors u (K x n) and v (K x m) on the device
 void factors_u(const double* delta_dev, size_t n, double gamma, size_t K, double2* u_dev,
