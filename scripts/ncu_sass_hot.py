@@ -13,7 +13,11 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-n
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
-data = [r for r in rows[2:] if len(r) == len(hdr) and r[0] != "Address"]
+data, _seen = [], set()
+for r in rows[2:]:  # the view repeats each SASS line once per matching function block
+    if len(r) == len(hdr) and r[0] != "Address" and r[0] not in _seen:
+        _seen.add(r[0])
+        data.append(r)
 S = ix["Warp Stall Sampling (All Samples)"]
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tot = sum(float(r[S]) for r in data)
