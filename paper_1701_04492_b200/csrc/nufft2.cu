@@ -1035,8 +1035,9 @@ __device__ __forceinline__ void fs_load_row(double2 (&v)[16], const double2* row
 template <class Bar>
 __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
                                             Bar gsync) {
-    gsync();  // the group's gathers from its buffer (its previous step) are done
-    block_fft_2l<-1>(v, buf, tid, T, gsync);
+    // the group's gathers from its buffer (its previous step) must be done before the
+    // first exchange write, not before the first-level DFT: wait there
+    block_fft_2l<-1>(v, buf, tid, T, gsync, [&] { gsync(); });
 #pragma unroll
     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
     gsync();  // X complete

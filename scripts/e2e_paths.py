@@ -38,3 +38,35 @@ pinned = med(lambda: p.execute_host_ptr(cp.data_ptr(), fp.data_ptr(), 1))
 alloc = med(lambda: np.zeros(n, np.complex128).fill(0))
 print(f"exec_host batch 1: pageable {pageable:.1f} ms, pinned {pinned:.1f} ms; "
       f"fresh 256 MiB output zero-filled {alloc:.1f} ms")
+
+# PCIe: one 256 MiB pinned copy each way, alone and both at once (two streams)
+d = torch.empty(n, dtype=torch.complex128, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+d2 = torch.empty_like(d)
+
+
+def h2d():
+    with torch.cuda.stream(s1):
+        d.copy_(cp, non_blocking=True)
+    s1.synchronize()
+
+
+def d2h():
+    with torch.cuda.stream(s2):
+        fp.copy_(d2, non_blocking=True)
+    s2.synchronize()
+
+
+def both():
+    with torch.cuda.stream(s1):
+        d.copy_(cp, non_blocking=True)
+    with torch.cuda.stream(s2):
+        fp.copy_(d2, non_blocking=True)
+    s1.synchronize()
+    s2.synchronize()
+
+
+gb = 16 * n / 1e9
+th, td, tb = med(h2d), med(d2h), med(both)
+print(f"PCIe pinned 256 MiB: H2D {th:.2f} ms ({gb / th * 1e3:.1f} GB/s), D2H {td:.2f} ms ({gb / td * 1e3:.1f} GB/s), "
+      f"both concurrently {tb:.2f} ms ({2 * gb / tb * 1e3:.1f} GB/s aggregate)")

@@ -112,3 +112,18 @@ def test_sampler_bit_identical_to_reference_sampler(port):
         assert np.array_equal(a.complex_vector(777), b.complex_vector(777))  # odd count: spare carried
         assert a() == b.normal()
         assert np.array_equal(a.uniform_vector(5, 0.0, 4096.0), b.uniform_vector(5, 0.0, 4096.0))
+
+
+def test_bench_fp64_roofline_block_from_committed_profile():
+    """bench.py's roofline.fp64 reads profiles/fp64.json (the committed ncu capture)."""
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    fp = json.load(open(os.path.join(ROOT, "profiles", "fp64.json")))
+    out = bench.fp64_roofline(fp, fp["n"], fp["K"], {"k2_pass1": 1.65, "k2_pass2": 2.19})
+    assert out and set(out["per_kernel"]) == {"k2_pass1", "k2_pass2"}
+    for v in out["per_kernel"].values():
+        assert 0.1 < v["frac_of_fp64_peak"] < 1.0
+    assert bench.fp64_roofline(fp, 1 << 22, fp["K"], {"k2_pass1": 1.0}) is None
+    assert bench.fp64_roofline(None, 1, 1, {}) is None
