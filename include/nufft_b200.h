@@ -158,6 +158,9 @@ int nufft_comm_info(const nufft_comm* comm, int* nranks, int* rank, int* device)
 int nufft_multi_term_range(size_t K, int nranks, int rank, size_t* r_begin, size_t* r_end); /* host-only */
 int nufft_plan2_exec_multi(const nufft_plan2* plan, const double* c_dev, double* f_dev, size_t batch,
                            nufft_comm* comm, int root, int mode, void* stream);
+/* host pointers (f written on the receiving ranks only; pageable memory is staged) */
+int nufft_plan2_exec_multi_host(const nufft_plan2* plan, const double* c, size_t len, double* f, size_t batch,
+                                nufft_comm* comm, int root, int mode);
 /* The pieces exec_multi is built from, for callers that bring their own
  * collective (e.g. torch.distributed): the partial over terms [r_begin, r_end)
  * of one vector in bucket order, the bucket-order ranges of the row chunks

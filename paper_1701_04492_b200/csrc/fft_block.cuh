@@ -151,7 +151,10 @@ struct FftShapeX : FftShape<L> {
     static constexpr int R3 = (FftShape<L>::STAGES == 3) ? R_LAST : 1;   // radix of the Ns=256 stage
     static constexpr int B3 = 16 / R3;                                    // its butterflies per thread
     static constexpr int T16_LEN = (FftShape<L>::STAGES >= 2) ? 16 * R2 : 16;
-    static constexpr int TB_LEN = (FftShape<L>::STAGES == 3) ? 4 * 256 : 0;  // stage-3 bases
+    // stage-3 bases w^(k 2^e), one 256-row per e < log2(R3): apply_pow_twiddles<R3> reads
+    // rows 0 .. log2(R3)-1 only (4 rows at L = 4096, 3 at 2048: 4 KiB less shared memory
+    // lets two k1_passA<2048> CTAs share an SM)
+    static constexpr int TB_LEN = (FftShape<L>::STAGES == 3) ? ilog2_c(R3) * 256 : 0;
     static constexpr int TW_LEN = T16_LEN + TB_LEN;  // shared twiddle storage (double2)
 };
 

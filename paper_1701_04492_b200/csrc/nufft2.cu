@@ -1035,9 +1035,11 @@ __device__ __forceinline__ void fs_load_row(double2 (&v)[16], const double2* row
 template <class Bar>
 __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
                                             Bar gsync) {
-    // the group's gathers from its buffer (its previous step) must be done before the
-    // first exchange write, not before the first-level DFT: wait there
-    block_fft_2l<-1>(v, buf, tid, T, gsync, [&] { gsync(); });
+    // the group's gathers from its buffer (its previous step) are done.  (Waiting only
+    // at the first exchange write, after the first-level DFT, measured slower here:
+    // pass 2 2.19 -> 2.44 ms.)
+    gsync();
+    block_fft_2l<-1>(v, buf, tid, T, gsync);
 #pragma unroll
     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
     gsync();  // X complete
@@ -1260,7 +1262,6 @@ __global__ void __launch_bounds__(512, 1)
         const bool has_next = row < n1;
         const int last = nt - 1;
         const int lastgrp = (S0 + last) & 1;  // group of the unit's last update
-        bool pre_loaded = false;              // v holds the next unit's first row
         for (int i = (grp - S0) & 1; i < nt; i += 2) {
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
@@ -1268,26 +1269,15 @@ __global__ void __launch_bounds__(512, 1)
                 if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
             }
-            // this group's next row (step i + 2) is in flight during the update — across the
-            // unit boundary too: the group that transforms the next unit's first row at the
-            // boundary loads it during its last update of this unit; a later row (step
-            // i + 2 kFsL2Prefetch, continuing into the next unit) is warmed in L2
+            // this group's next row (step i + 2) is in flight during the update; a later
+            // one (step i + 2 kFsL2Prefetch) is warmed in L2.  (Loading / prefetching the
+            // next unit's first row across the unit boundary measured slower: 2.44 vs 2.48.)
             have = i + 2 < nt;
-            if (have) {
-                fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
-            } else if (has_next && grp != lastgrp) {
-                fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
-                pre_loaded = true;
-            }
-            if (tid == 0) {
-                const int ia = i + 2 * kFsL2Prefetch;  // step to warm (>= nt: the next unit's)
-                const long long prow = ia < nt ? urow : row;
-                const int prr = ia < nt ? rr - 2 * kFsL2Prefetch : last - (ia - nt);
-                if ((ia < nt || (has_next && ia - nt < nt)) && (prow & 1) == 0) {
-                    const void* nxt = Y + y_index(prr, N, p.log_n2, prow, 0);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
-                                 "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
-                }
+            if (have) fs_load_row(v, Y + y_index(rr - 2, N, p.log_n2, urow, 0), tid);
+            if (tid == 0 && i + 2 * kFsL2Prefetch < nt && (urow & 1) == 0) {
+                const void* nxt = Y + y_index(rr - 2 * kFsL2Prefetch, N, p.log_n2, urow, 0);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
+                             "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
             }
             if (i > 0) {  // the other group's update of step i-1 is done
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
@@ -1340,7 +1330,7 @@ __global__ void __launch_bounds__(512, 1)
         pre = false;
         if (grp != lastgrp) {
             if (has_next) {
-                if (!pre_loaded) fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
+                fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
                 pre = true;
             }

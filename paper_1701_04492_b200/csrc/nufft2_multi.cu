@@ -230,6 +230,24 @@ int nufft_multi_term_range(size_t K, int nranks, int rank, size_t* r_begin, size
     });
 }
 
+int nufft_plan2_exec_multi_host(const nufft_plan2* plan, const double* c, size_t len, double* f, size_t batch,
+                                nufft_comm* comm, int root, int mode) {
+    return guard([&] {
+        if (!plan || !comm) nb::throw_invalid("exec_multi: null argument");
+        const nb::CorePlan& p = plan->core;
+        if (len != p.n) nb::throw_invalid("exec_nufft2: length mismatch");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = cudaStreamPerThread;
+        nb::DevBuf din(16 * p.n * batch, s), dout(16 * p.n * batch, s);
+        nb::h2d(din.get(), c, 16 * p.n * batch, s);
+        const int rc = nufft_plan2_exec_multi(plan, din.as<double>(), dout.as<double>(), batch, comm, root, mode, s);
+        if (rc != NUFFT_OK) throw nb::Error(rc, nb::last_error());
+        const bool receives = mode == NUFFT_MULTI_ALLREDUCE || comm->rank == root;
+        if (receives) nb::d2h(f, dout.get(), 16 * p.n * batch, s);
+        else NB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int nufft_plan2_exec_terms_sorted(const nufft_plan2* plan, const double* c_dev, double* fs_dev, size_t r_begin,
                                   size_t r_end, void* stream) {
     return guard([&] {

@@ -399,9 +399,8 @@ __global__ void __launch_bounds__(512, 1)
                     double2 v[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
-                    // this group's gathers from buf (its previous step) must be done before the
-                    // first exchange write: wait there, after the first-level DFT
-                    block_fft_2l<-1>(v, buf, tid, T, gsync, [&] { gsync(); });
+                    gsync();  // this group's gathers from buf (its previous step) are done
+                    block_fft_2l<-1>(v, buf, tid, T, gsync);
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
                     gsync();  // X complete

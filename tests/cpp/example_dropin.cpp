@@ -91,6 +91,16 @@ int main() {
     auto pd = nufft::plan_nufft2d2(xx, y, 16, 16, 1e-9);
     auto fd = nufft::exec_nufft2d2(pd, C);
     if (fd.size() != 300 || f1.size() != n) return 1;
+    // multi-GPU drop-in (include/nufft/multi_gpu.hpp) on a one-rank communicator: the
+    // in-library r-split with its chunked NCCL reduce equals the single-GPU exec
+    {
+        nufft::Communicator comm(nufft::make_comm_id(), 1, 0, 0);
+        if (comm.nranks() != 1 || comm.rank() != 0) return std::printf("comm info\n"), 1;
+        const auto fm = nufft::exec_nufft2(plan, c, comm);
+        if (fm != f) return std::printf("exec_multi != exec\n"), 1;
+        const auto [r0, r1] = nufft::term_range(plan.rank(), 4, 1);
+        if (r0 != 5 || r1 != 10) return std::printf("term_range\n"), 1;
+    }
     std::printf("OK rank=%zu worst=%.3g\n", plan.rank(), worst);
     return 0;
 }
