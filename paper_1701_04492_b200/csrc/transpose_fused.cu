@@ -401,10 +401,12 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
                     }
                     v[q] = acc;
                 }
-                gsync();  // terms read before stage 1 reuses buf
                 if constexpr (F2L) {
-                    block_fft_2l<-1>(v, buf, tid, T, gsync);
+                    // the terms must have been read by every bin sum before the exchange
+                    // first writes buf: wait there, after the first-level DFT
+                    block_fft_2l<-1>(v, buf, tid, T, gsync, [&] { gsync(); });
                 } else {
+                    gsync();  // terms read before stage 1 reuses buf
                     block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
                 }
                 double2* out = Z + (long long)(r - p.r0) * N + (row << p.log_n2);
