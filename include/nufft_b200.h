@@ -161,6 +161,13 @@ int nufft_plan2_exec_multi(const nufft_plan2* plan, const double* c_dev, double*
 /* host pointers (f written on the receiving ranks only; pageable memory is staged) */
 int nufft_plan2_exec_multi_host(const nufft_plan2* plan, const double* c, size_t len, double* f, size_t batch,
                                 nufft_comm* comm, int root, int mode);
+/* Type I (the transpose core) over G GPUs: rank g evaluates terms [K g/G, K (g+1)/G)
+ * (both passes) and the partial f are summed (one reduce at the end; pass B writes f by
+ * columns).  exec_terms: one rank's partial, for callers with their own collective.     */
+int nufft_plan1_exec_terms(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
+                           size_t r_begin, size_t r_end, void* stream);
+int nufft_plan1_exec_multi(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
+                           nufft_comm* comm, int root, int mode, void* stream);
 /* The pieces exec_multi is built from, for callers that bring their own
  * collective (e.g. torch.distributed): the partial over terms [r_begin, r_end)
  * of one vector in bucket order, the bucket-order ranges of the row chunks

@@ -110,6 +110,8 @@ _SIGS = {
     "nufft_multi_term_range": (_i, [_sz, _i, _i, C.POINTER(_sz), C.POINTER(_sz)]),
     "nufft_plan2_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
     "nufft_plan2_exec_multi_host": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i]),
+    "nufft_plan1_exec_terms": (_i, [_vp, _vp, _vp, _sz, _sz, _sz, _vp]),
+    "nufft_plan1_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
     "nufft_plan2_exec_terms_sorted": (_i, [_vp, _vp, _vp, _sz, _sz, _vp]),
     "nufft_plan2_reduce_chunks": (_i, [_vp, _i, _vp]),
     "nufft_plan2_unpermute": (_i, [_vp, _vp, _vp, _sz, _vp]),

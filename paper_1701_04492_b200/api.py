@@ -336,6 +336,17 @@ class Plan1(_PlanBase):
     def execute_device(self, c_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
         _check(lib().nufft_plan1_exec(self._h, c_ptr, f_ptr, batch, stream or None))
 
+    def execute_terms_device(self, c_ptr: int, f_ptr: int, r_begin: int, r_end: int,
+                             batch: int = 1, stream: int = 0) -> None:
+        """Partial sum over the terms [r_begin, r_end) (one rank's share)."""
+        _check(lib().nufft_plan1_exec_terms(self._h, c_ptr, f_ptr, batch, r_begin, r_end, stream or None))
+
+    def execute_multi_device(self, c_ptr: int, f_ptr: int, comm, batch: int = 1, stream: int = 0,
+                             root: int = 0, allreduce: bool = False) -> None:
+        """r-split over an NCCL communicator (parallel.NcclComm); f complete on `root`."""
+        _check(lib().nufft_plan1_exec_multi(self._h, c_ptr, f_ptr, batch, comm.handle, root,
+                                            1 if allreduce else 0, stream or None))
+
 
 class Plan3(_PlanBase):
     """Type-III plan (transforms.hpp:308-319)."""

@@ -176,14 +176,19 @@ void conj_copy(const double2* in, double2* out, size_t n, cudaStream_t s) {
 }
 
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
-                    cudaStream_t s) {
-    if (p.fused) return exec_transpose_fused(p, g, f, batch, s);
+                    cudaStream_t s, size_t r_begin, size_t r_end) {
+    if (p.fused) return exec_transpose_fused(p, g, f, batch, s, nullptr, r_begin, r_end);
     ensure_bessel_constants(p.device);
     if (!p.have_bins) throw Error(kInternal, "transpose core: plan has no bins");
     const size_t N = p.n;
     DevBuf bins(sizeof(double2) * N, s);
+    const size_t r1 = std::min(r_end, p.K);
+    if (r1 <= r_begin) {
+        NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * N * batch, s));
+        return;
+    }
     for (size_t b = 0; b < batch; ++b) {
-        for (size_t r = 0; r < p.K; ++r) {
+        for (size_t r = r_begin; r < r1; ++r) {
             k1_scatter<<<blocks(N), 256, 0, s>>>(g + b * N, p.bk.sort_perm.as<int>(),
                                                  p.bk.bin_off.as<int>(), p.ax.delta.as<double>(),
                                                  bins.as<double2>(), (long long)N, (int)r,
@@ -191,7 +196,7 @@ void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batc
             NB_LAUNCH();
             fft_exec(bins.as<double2>(), bins.as<double2>(), N, 1, -1, s, p.device);
             k1_accum<<<blocks(N), 256, 0, s>>>(bins.as<double2>(), f + b * N, (long long)N, (int)r,
-                                               r == 0 ? 1 : 0, p.uniform ? 1 : 0);
+                                               r == r_begin ? 1 : 0, p.uniform ? 1 : 0);
             NB_LAUNCH();
         }
     }

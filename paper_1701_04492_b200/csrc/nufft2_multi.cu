@@ -248,6 +248,46 @@ int nufft_plan2_exec_multi_host(const nufft_plan2* plan, const double* c, size_t
     });
 }
 
+int nufft_plan1_exec_terms(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
+                           size_t r_begin, size_t r_end, void* stream) {
+    return guard([&] {
+        const nb::CorePlan& p = plan->core;
+        NB_CUDA(cudaSetDevice(p.device));
+        if (r_end > p.K) r_end = p.K;
+        nb::exec_transpose(p, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev), batch,
+                           stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread, r_begin, r_end);
+        if (r_end > r_begin) nb::fft_count(p.n, (r_end - r_begin) * batch);
+    });
+}
+
+// Type I over G GPUs: rank g runs the transpose core on its r-range (both passes; pass B
+// accumulates v_r X_r of those terms), and the natural-order partial sums are reduced once
+// (pass B writes f column by column, so there is no contiguous chunk to reduce early).
+int nufft_plan1_exec_multi(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
+                           nufft_comm* comm, int root, int mode, void* stream) {
+    return guard([&] {
+        if (!plan || !comm) nb::throw_invalid("exec_multi: null argument");
+        if (mode != NUFFT_MULTI_REDUCE && mode != NUFFT_MULTI_ALLREDUCE) nb::throw_invalid("exec_multi: mode");
+        if (root < 0 || root >= comm->nranks) nb::throw_invalid("exec_multi: root out of range");
+        const nb::CorePlan& p = plan->core;
+        if (p.device != comm->device) nb::throw_invalid("exec_multi: plan and communicator on different devices");
+        NB_CUDA(cudaSetDevice(p.device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        size_t r0, r1;
+        nb::term_range(p.K, comm->nranks, comm->rank, &r0, &r1);
+        nb::DevBuf part(sizeof(double2) * p.n * batch, s);
+        nb::exec_transpose(p, reinterpret_cast<const double2*>(c_dev), part.as<double2>(), batch, s, r0, r1);
+        const nb::NcclApi& api = nb::nccl();
+        if (mode == NUFFT_MULTI_ALLREDUCE)
+            nb::nccl_check(api.all_reduce(part.get(), f_dev, 2 * p.n * batch, ncclDouble, ncclSum, comm->comm, s),
+                           "ncclAllReduce");
+        else
+            nb::nccl_check(api.reduce(part.get(), f_dev, 2 * p.n * batch, ncclDouble, ncclSum, root, comm->comm, s),
+                           "ncclReduce");
+        if (r1 > r0) nb::fft_count(p.n, (r1 - r0) * batch);
+    });
+}
+
 int nufft_plan2_exec_terms_sorted(const nufft_plan2* plan, const double* c_dev, double* fs_dev, size_t r_begin,
                                   size_t r_end, void* stream) {
     return guard([&] {

@@ -15,6 +15,8 @@
 // delta from x exactly as the reference does (transforms.hpp:60-64,84-86).
 #pragma once
 
+#include <cstdint>
+
 #include <cstddef>
 #include <memory>
 #include <vector>
@@ -126,11 +128,12 @@ void exec_type2_pass2_rows(const CorePlan& p, const double2* Y, double2* f, size
 void unpermute(const CorePlan& p, const double2* fs, double2* f, size_t batch, cudaStream_t s);
 // F2~^T g = sum_r v_r .* F scatter_t(u_r .* g)   (transforms.hpp:206-221)
 void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batch,
-                    cudaStream_t s);
+                    cudaStream_t s, size_t r_begin = 0, size_t r_end = SIZE_MAX);
 // fused two-pass form of exec_transpose for power-of-two N (transpose_fused.cu);
 // ev as for exec_type2
 void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_t batch,
-                          cudaStream_t s, cudaEvent_t* ev = nullptr);
+                          cudaStream_t s, cudaEvent_t* ev = nullptr, size_t r_begin = 0,
+                          size_t r_end = SIZE_MAX);
 void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s);

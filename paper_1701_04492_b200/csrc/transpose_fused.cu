@@ -918,10 +918,14 @@ void dispatch_passB(int L, const double2* Z, double2* f, const CorePlan& pl, int
 }  // namespace
 
 void exec_transpose_fused(const CorePlan& pl, const double2* g, double2* f, size_t batch,
-                          cudaStream_t s, cudaEvent_t* ev) {
+                          cudaStream_t s, cudaEvent_t* ev, size_t r_begin, size_t r_end) {
     ensure_bessel_constants(pl.device);
     const size_t N = pl.n;
-    const int r0 = 0, r1 = (int)pl.K;
+    const int r0 = (int)r_begin, r1 = (int)std::min(r_end, pl.K);
+    if (r1 <= r0) {  // no terms: zero output
+        NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * N * batch, s));
+        return;
+    }
     DevBuf Z(sizeof(double2) * N * (size_t)(r1 - r0), s);
     const int L1 = 1 << pl.bk.log_n1, L2 = 1 << pl.bk.log_n2;
     for (size_t b = 0; b < batch; ++b) {

@@ -190,3 +190,33 @@ def test_rsplit_two_gloo_ranks_product_partials(nb):
     assert all(p.exitcode == 0 for p in procs)
     errs = dict(q.get(timeout=5) for _ in range(2))
     assert max(errs.values()) <= 1e-14, errs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1 << 16, 1 << 22, 3000])
+def test_type1_term_shards_and_single_rank_multi(nb, n):
+    """Type-I r-split: term-range partials (transpose core, both passes) sum to the full
+    transform, and exec_multi over a one-rank NCCL communicator equals exec."""
+    import torch
+    from paper_1701_04492_b200.parallel import NcclComm, unique_id
+    rng = nb.GaussianSampler(n + 1)
+    w = np.clip(np.arange(n) + rng.uniform_vector(n, -0.5, 0.5), 0.0, float(n))
+    p = nb.plan_nufft1(w, 1e-12, device=0)
+    c = torch.from_numpy(rng.complex_vector(n)).cuda()
+    full = torch.empty_like(c)
+    p.execute_device(c.data_ptr(), full.data_ptr())
+    K = p.rank()
+    acc = torch.zeros_like(c)
+    for g in range(3):
+        r0, r1 = term_range(K, 3, g)
+        part = torch.empty_like(c)
+        p.execute_terms_device(c.data_ptr(), part.data_ptr(), r0, r1)
+        acc += part
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(acc - full) / torch.linalg.norm(full)).item() <= 1e-14
+    comm = NcclComm(unique_id(), 1, 0, 0)
+    got = torch.full_like(c, float("nan"))
+    p.execute_multi_device(c.data_ptr(), got.data_ptr(), comm)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(full))
+    comm.close()
