@@ -213,16 +213,16 @@ __global__ void __launch_bounds__(L2 / 16, 1)
 // (4 columns, advanced by one multiply by h_j per term) and h_j (2 columns),
 // 17 samples x 6 = 102 columns per thread; each worker keeps one padded
 // buffer (terms, then FFT exchange) and its bin table in shared memory.
-template <int L2>
+template <int L2, int NW = 2>
 struct PassATmShape {
     static constexpr int G = L2 / 16;
     static constexpr int QA = 17;
     static constexpr int CAP = QA * G;
     static constexpr int COL_Q = 0, COL_H = 4 * QA;  // 68 + 34 = 102 columns
-    static constexpr size_t SMEM = sizeof(double2) * (2 * padded_len(L2) + FftShapeX<L2>::TW_LEN) +
-                                   2 * sizeof(unsigned) * L2;
-    static_assert(SMEM <= kSmemLimit, "pass A (two workers) shared memory");
-    static_assert((2 * G / 32 + 3) / 4 * 6 * QA <= 512, "TMEM columns");
+    static constexpr size_t SMEM = sizeof(double2) * (NW * padded_len(L2) + FftShapeX<L2>::TW_LEN) +
+                                   NW * sizeof(unsigned) * L2;
+    static_assert(SMEM <= kSmemLimit, "pass A (row workers) shared memory");
+    static_assert((NW * G + 127) / 128 * 6 * QA <= 512, "TMEM columns");
 };
 
 // F2L (L2 = 4096): the row FFT is block_fft_2l; output k2 of register q is
@@ -231,13 +231,13 @@ struct PassATmShape {
 // engine — the z values are staged conflict-free in the exchange buffer in the
 // order (b, warp, u, e) and one 5-D cp.async.bulk.tensor store writes the 64 KiB
 // Z row (dims: e pair = 4 doubles, u, warp, b, rr N1 + row), as in k2_pass1_tma.
-template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false>
-__global__ void __launch_bounds__(2 * (L2 / 16), 1)
+template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false, int NW = 2>
+__global__ void __launch_bounds__(NW * (L2 / 16), 1)
     k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p,
                 const __grid_constant__ CUtensorMap zmap) {
     static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
     static_assert(!TMA || F2L, "TMA store needs the two-level output order");
-    using S = PassATmShape<L2>;
+    using S = PassATmShape<L2, NW>;
     constexpr int G = S::G;
     constexpr int QA = S::QA;
     constexpr int CAP = S::CAP;
@@ -246,10 +246,10 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
     const int grp = threadIdx.x / G;
     const int tid = threadIdx.x - grp * G;
     double2* buf = smem + grp * padded_len(L2);
-    double2* tw = smem + 2 * padded_len(L2);
+    double2* tw = smem + NW * padded_len(L2);
     unsigned* bo = reinterpret_cast<unsigned*>(tw + FftShapeX<L2>::TW_LEN) + grp * L2;
     unsigned short* bo16 = reinterpret_cast<unsigned short*>(bo);
-    twiddle_table_build<L2>(tw, threadIdx.x, 2 * G);
+    twiddle_table_build<L2>(tw, threadIdx.x, NW * G);
     Twiddles<L2> T;
     twiddle_init<L2>(T, tw, tid);
     if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(2 * (L2 / 16), 1)
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
     const unsigned mask = (1u << p.log_n2) - 1u;
-    for (long long row = 2ll * blockIdx.x + grp; row < n1; row += 2ll * gridDim.x) {
+    for (long long row = (long long)NW * blockIdx.x + grp; row < n1; row += (long long)NW * gridDim.x) {
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         if (beg == end) {  // empty row: Z_r[row][:] = 0
             for (int r = p.r0; r < p.r1; ++r) {
@@ -829,7 +829,7 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
     p.perm = pl.bk.perm.as<int>();
     p.rowoff = pl.bk.rowoff.as<int>();
     for (size_t r = 0; r < pl.series_deg.size() && r < (size_t)kRankCap; ++r) p.deg[r] = pl.series_deg[r];
-    if constexpr (L2 == 4096) {  // at 2048 two single-worker CTAs per SM are faster (1.44 vs 1.63 ms, type I at 2^22)
+    if constexpr (L2 == 4096) {
         constexpr size_t SMT = PassATmShape<L2>::SMEM;
         // two-level row FFT; Z rows stored by TMA (LSU stores when the tensor map
         // cannot describe Z)
@@ -841,6 +841,20 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
         const long long rows = 1ll << pl.bk.log_n1;
         const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
         fnt<<<gridt, 2 * (L2 / 16), SMT, s>>>(g, Z, p, zmap);
+        NB_LAUNCH();
+        return;
+    }
+    if constexpr (L2 == 2048) {
+        // four row workers of 128 threads (16 warps/SM) with the per-sample state in TMEM:
+        // the cfg4 inner type-I transforms 30.3 -> 27.1 ms per type-III exec (a jittered
+        // type I at 2^22: 1.44 -> 1.47 ms); two workers measured 1.63 ms
+        using S4 = PassATmShape<L2, 4>;
+        auto f4 = pl.uniform ? k1_passA_tm<L2, true, false, false, 4> : k1_passA_tm<L2, false, false, false, 4>;
+        CUtensorMap zmap{};
+        set_smem(f4, S4::SMEM);
+        const long long rows = 1ll << pl.bk.log_n1;
+        const int grid4 = (int)std::min<long long>((rows + 3) / 4, (long long)ctx.sms);
+        f4<<<grid4, 4 * (L2 / 16), S4::SMEM, s>>>(g, Z, p, zmap);
         NB_LAUNCH();
         return;
     }
