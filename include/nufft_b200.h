@@ -168,6 +168,19 @@ int nufft_plan1_exec_terms(const nufft_plan1* plan, const double* c_dev, double*
                            size_t r_begin, size_t r_end, void* stream);
 int nufft_plan1_exec_multi(const nufft_plan1* plan, const double* c_dev, double* f_dev, size_t batch,
                            nufft_comm* comm, int root, int mode, void* stream);
+/* Type III over G GPUs: rank g takes the outer terms [K g/G, K (g+1)/G) (inner type-I
+ * transforms, beta dot products, the partial epilogue) and the partial f are summed.   */
+int nufft_plan3_exec_terms(const nufft_plan3* plan, const double* c_dev, double* f_dev, size_t batch,
+                           size_t r_begin, size_t r_end, void* stream);
+int nufft_plan3_exec_multi(const nufft_plan3* plan, const double* c_dev, double* f_dev, size_t batch,
+                           nufft_comm* comm, int root, int mode, void* stream);
+/* 2D over G GPUs: rank g takes the row-stage terms r1 in [Kx g/G, Kx (g+1)/G) (its row stage
+ * and its Kx/G x Ky column steps) and the partial f are summed (fused plans: power-of-two
+ * m, n in [16, 4096]; other plans run whole on the root).                                  */
+int nufft_plan2d2_exec_terms(const nufft_plan2d* plan, const double* C_dev, double* f_dev, size_t batch,
+                             size_t r1_begin, size_t r1_end, void* stream);
+int nufft_plan2d2_exec_multi(const nufft_plan2d* plan, const double* C_dev, double* f_dev, size_t batch,
+                             nufft_comm* comm, int root, int mode, void* stream);
 /* The pieces exec_multi is built from, for callers that bring their own
  * collective (e.g. torch.distributed): the partial over terms [r_begin, r_end)
  * of one vector in bucket order, the bucket-order ranges of the row chunks

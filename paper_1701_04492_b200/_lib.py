@@ -112,6 +112,10 @@ _SIGS = {
     "nufft_plan2_exec_multi_host": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i]),
     "nufft_plan1_exec_terms": (_i, [_vp, _vp, _vp, _sz, _sz, _sz, _vp]),
     "nufft_plan1_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
+    "nufft_plan3_exec_terms": (_i, [_vp, _vp, _vp, _sz, _sz, _sz, _vp]),
+    "nufft_plan3_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
+    "nufft_plan2d2_exec_terms": (_i, [_vp, _vp, _vp, _sz, _sz, _sz, _vp]),
+    "nufft_plan2d2_exec_multi": (_i, [_vp, _vp, _vp, _sz, _vp, _i, _i, _vp]),
     "nufft_plan2_exec_terms_sorted": (_i, [_vp, _vp, _vp, _sz, _sz, _vp]),
     "nufft_plan2_reduce_chunks": (_i, [_vp, _i, _vp]),
     "nufft_plan2_unpermute": (_i, [_vp, _vp, _vp, _sz, _vp]),

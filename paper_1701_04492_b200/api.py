@@ -377,6 +377,17 @@ class Plan3(_PlanBase):
     def execute_device(self, c_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
         _check(lib().nufft_plan3_exec(self._h, c_ptr, f_ptr, batch, stream or None))
 
+    def execute_terms_device(self, c_ptr: int, f_ptr: int, r_begin: int, r_end: int,
+                             batch: int = 1, stream: int = 0) -> None:
+        """Partial sum over the outer terms [r_begin, r_end) (one rank's share)."""
+        _check(lib().nufft_plan3_exec_terms(self._h, c_ptr, f_ptr, batch, r_begin, r_end, stream or None))
+
+    def execute_multi_device(self, c_ptr: int, f_ptr: int, comm, batch: int = 1, stream: int = 0,
+                             root: int = 0, allreduce: bool = False) -> None:
+        """Outer-term split over an NCCL communicator (parallel.NcclComm)."""
+        _check(lib().nufft_plan3_exec_multi(self._h, c_ptr, f_ptr, batch, comm.handle, root,
+                                            1 if allreduce else 0, stream or None))
+
 
 class Plan2D(_PlanBase):
     """2D type-II plan (transform2d.hpp:51-59)."""
@@ -417,6 +428,17 @@ class Plan2D(_PlanBase):
 
     def execute_device(self, C_ptr: int, f_ptr: int, batch: int = 1, stream: int = 0) -> None:
         _check(lib().nufft_plan2d2_exec(self._h, C_ptr, f_ptr, batch, stream or None))
+
+    def execute_terms_device(self, C_ptr: int, f_ptr: int, r1_begin: int, r1_end: int,
+                             batch: int = 1, stream: int = 0) -> None:
+        """Partial sum over the row-stage terms [r1_begin, r1_end) (one rank's share)."""
+        _check(lib().nufft_plan2d2_exec_terms(self._h, C_ptr, f_ptr, batch, r1_begin, r1_end, stream or None))
+
+    def execute_multi_device(self, C_ptr: int, f_ptr: int, comm, batch: int = 1, stream: int = 0,
+                             root: int = 0, allreduce: bool = False) -> None:
+        """r1 split over an NCCL communicator (parallel.NcclComm)."""
+        _check(lib().nufft_plan2d2_exec_multi(self._h, C_ptr, f_ptr, batch, comm.handle, root,
+                                              1 if allreduce else 0, stream or None))
 
 
 class GaussianSampler:

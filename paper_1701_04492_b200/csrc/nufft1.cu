@@ -137,31 +137,43 @@ __global__ void k3_beta_dot_final(const double2* __restrict__ part, int r0, int 
 // series values (as in the type-II pass 2, nufft2.cu).
 __global__ void k3_epilogue(const double2* __restrict__ Y, const double2* __restrict__ D,
                             const int* __restrict__ ord_perm, const unsigned* __restrict__ ord_key,
-                            const double* __restrict__ ord_delta, long long n, int K, int deg_top0, int deg_top1,
-                            int uniform, double2* __restrict__ f) {
+                            const double* __restrict__ ord_delta, long long n, int r0, int r1, int deg_top0,
+                            int deg_top1, int uniform, double2* __restrict__ f) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned key = ord_key[i];
     const long long t = key & 0x7fffffffu;
     const bool beta = (key >> 31) != 0;  // s = N, t = 0: the node at 1 (transforms.hpp:345-350)
     const int j = ord_perm[i];
-    if (uniform) {
+    if (uniform) {  // K = 1, u = v = 1
         f[j] = beta ? D[0] : Y[t];
         return;
     }
+    // Y holds the terms [r0, r1) (slice r - r0); D is indexed by the absolute r
     const double h = half_phase(ord_delta[i]);
     const double w = h * h;
-    double g1 = bessel_g_rt(K, deg_top1, w);      // g_K
-    double g0 = bessel_g_rt(K - 1, deg_top0, w);  // g_{K-1}
+    double g1 = bessel_g_rt(r1, deg_top1, w);      // g_{r1}
+    double g0 = bessel_g_rt(r1 - 1, deg_top0, w);  // g_{r1-1}
     double2 acc = make_double2(0.0, 0.0);
-    for (int r = K - 1; r >= 0; --r) {
-        const double2 z = beta ? D[r] : __ldg(Y + (long long)r * n + t);
+    for (int r = r1 - 1; r >= r0; --r) {
+        const double2 z = beta ? D[r] : __ldg(Y + (long long)(r - r0) * n + t);
         const double ax = acc.x;
         acc.x = __fma_rn(g0, z.x, -h * acc.y);
         acc.y = __fma_rn(g0, z.y, h * ax);
         const double gm1 = __fma_rn((double)r, g0, -w * g1);  // g_{r-1}
         g1 = g0;
         g0 = gm1;
+    }
+    if (r0 > 0) {  // a partial term range (multi-GPU): restore (ih)^r0
+        double hr = 1.0;
+        for (int m = 0; m < r0; ++m) hr *= h;
+        acc = cscale(acc, hr);
+        switch (r0 & 3) {
+            case 1: acc = make_double2(-acc.y, acc.x); break;
+            case 2: acc = make_double2(-acc.x, -acc.y); break;
+            case 3: acc = make_double2(acc.y, -acc.x); break;
+            default: break;
+        }
     }
     double sn, cs;
     sincos(2.0 * h, &sn, &cs);
@@ -202,33 +214,40 @@ void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batc
     }
 }
 
-void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s) {
+void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s, size_t r_begin,
+                size_t r_end) {
     ensure_bessel_constants(p.a.device);
     const size_t N = p.a.n;
     const size_t K = p.a.K;
+    const size_t r0 = r_begin, r1 = std::min(r_end, K);
+    if (r1 <= r0) {
+        NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * N * batch, s));
+        return;
+    }
+    const size_t nt = r1 - r0;
     const int uni = p.a.uniform ? 1 : 0;
-    // y_r = F1~(v_r .* c) for the first family (K inner type-I transforms), kept
-    // for the single sample-ordered epilogue; the beta family reduces to K dot
-    // products (D_r) whenever B is non-trivial
-    DevBuf scaled(sizeof(double2) * N, s), Y(sizeof(double2) * N * K, s), D(sizeof(double2) * K, s);
+    // y_r = F1~(v_r .* c) for the first family (the inner type-I transforms of terms
+    // [r0, r1)), kept for the single sample-ordered epilogue; the beta family reduces to
+    // dot products (D_r) whenever B is non-trivial
+    DevBuf scaled(sizeof(double2) * N, s), Y(sizeof(double2) * N * nt, s), D(sizeof(double2) * K, s);
     DevBuf part(p.btrivial ? 16 : sizeof(double2) * kDotBlocks * kDotTerms, s);
-    const int deg0 = bessel_series_degree_rel(p.a.gamma_factors, (int)K - 1);
-    const int deg1 = bessel_series_degree_rel(p.a.gamma_factors, (int)K);
+    const int deg0 = bessel_series_degree_rel(p.a.gamma_factors, (int)r1 - 1);
+    const int deg1 = bessel_series_degree_rel(p.a.gamma_factors, (int)r1);
     for (size_t b = 0; b < batch; ++b) {
         const double2* cb = c + b * N;
-        for (size_t r = 0; r < K; ++r) {
+        for (size_t r = r0; r < r1; ++r) {
             k3_scale<<<blocks(N), 256, 0, s>>>(cb, p.omega.as<double>(), scaled.as<double2>(), (long long)N,
                                                (int)r, uni);
             NB_LAUNCH();
-            exec_transpose(p.inner, scaled.as<double2>(), Y.as<double2>() + r * N, 1, s);
+            exec_transpose(p.inner, scaled.as<double2>(), Y.as<double2>() + (r - r0) * N, 1, s);
         }
         if (!p.btrivial) {
-            for (size_t r0 = 0; r0 < K; r0 += kDotTerms) {
-                const int nr = (int)std::min<size_t>(kDotTerms, K - r0);
-                k3_beta_dot_part<<<kDotBlocks, kDotThreads, 0, s>>>(cb, p.omega.as<double>(), (long long)N, (int)r0,
+            for (size_t q0 = r0; q0 < r1; q0 += kDotTerms) {
+                const int nr = (int)std::min<size_t>(kDotTerms, r1 - q0);
+                k3_beta_dot_part<<<kDotBlocks, kDotThreads, 0, s>>>(cb, p.omega.as<double>(), (long long)N, (int)q0,
                                                                      nr, uni, part.as<double2>());
                 NB_LAUNCH();
-                k3_beta_dot_final<<<1, 32, 0, s>>>(part.as<double2>(), (int)r0, nr, D.as<double2>());
+                k3_beta_dot_final<<<1, 32, 0, s>>>(part.as<double2>(), (int)q0, nr, D.as<double2>());
                 NB_LAUNCH();
             }
         } else {
@@ -236,7 +255,7 @@ void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch,
         }
         k3_epilogue<<<blocks(N), 256, 0, s>>>(Y.as<double2>(), D.as<double2>(), p.ord_perm.as<int>(),
                                               p.ord_key.as<unsigned>(), p.ord_delta.as<double>(), (long long)N,
-                                              (int)K, deg0, deg1, uni, f + b * N);
+                                              (int)r0, (int)r1, deg0, deg1, uni, f + b * N);
         NB_LAUNCH();
     }
 }

@@ -288,6 +288,91 @@ int nufft_plan1_exec_multi(const nufft_plan1* plan, const double* c_dev, double*
     });
 }
 
+int nufft_plan3_exec_terms(const nufft_plan3* plan, const double* c_dev, double* f_dev, size_t batch,
+                           size_t r_begin, size_t r_end, void* stream) {
+    return guard([&] {
+        const nb::Plan3State& st = plan->st;
+        NB_CUDA(cudaSetDevice(st.a.device));
+        if (r_end > st.a.K) r_end = st.a.K;
+        nb::exec_type3(st, reinterpret_cast<const double2*>(c_dev), reinterpret_cast<double2*>(f_dev), batch,
+                       stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread, r_begin, r_end);
+        if (r_end > r_begin) nb::fft_count(st.a.n, (r_end - r_begin) * st.inner.K * batch);
+    });
+}
+
+// Type III over G GPUs: rank g takes the outer terms q in [K g/G, K (g+1)/G) (their inner
+// type-I transforms, beta dot products and the epilogue's partial Horner sum), and the
+// partial f are summed once (shard the (q, r) pairs, reduce f).
+int nufft_plan3_exec_multi(const nufft_plan3* plan, const double* c_dev, double* f_dev, size_t batch,
+                           nufft_comm* comm, int root, int mode, void* stream) {
+    return guard([&] {
+        if (!plan || !comm) nb::throw_invalid("exec_multi: null argument");
+        if (mode != NUFFT_MULTI_REDUCE && mode != NUFFT_MULTI_ALLREDUCE) nb::throw_invalid("exec_multi: mode");
+        if (root < 0 || root >= comm->nranks) nb::throw_invalid("exec_multi: root out of range");
+        const nb::Plan3State& st = plan->st;
+        if (st.a.device != comm->device) nb::throw_invalid("exec_multi: plan and communicator on different devices");
+        NB_CUDA(cudaSetDevice(st.a.device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        size_t r0, r1;
+        nb::term_range(st.a.K, comm->nranks, comm->rank, &r0, &r1);
+        nb::DevBuf part(sizeof(double2) * st.a.n * batch, s);
+        nb::exec_type3(st, reinterpret_cast<const double2*>(c_dev), part.as<double2>(), batch, s, r0, r1);
+        const nb::NcclApi& api = nb::nccl();
+        if (mode == NUFFT_MULTI_ALLREDUCE)
+            nb::nccl_check(api.all_reduce(part.get(), f_dev, 2 * st.a.n * batch, ncclDouble, ncclSum, comm->comm, s),
+                           "ncclAllReduce");
+        else
+            nb::nccl_check(api.reduce(part.get(), f_dev, 2 * st.a.n * batch, ncclDouble, ncclSum, root, comm->comm, s),
+                           "ncclReduce");
+        if (r1 > r0) nb::fft_count(st.a.n, (r1 - r0) * st.inner.K * batch);
+    });
+}
+
+int nufft_plan2d2_exec_terms(const nufft_plan2d* plan, const double* C_dev, double* f_dev, size_t batch,
+                             size_t r1_begin, size_t r1_end, void* stream) {
+    return guard([&] {
+        const nb::Plan2DState& st = plan->st;
+        if (!st.fused) nb::throw_invalid("exec_terms (2D): fused plans only (power-of-two m, n in [16, 4096])");
+        NB_CUDA(cudaSetDevice(st.device));
+        nb::exec_2d_fused(st, reinterpret_cast<const double2*>(C_dev), reinterpret_cast<double2*>(f_dev), batch,
+                          stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread, r1_begin, r1_end);
+    });
+}
+
+// 2D over G GPUs: rank g takes the row-stage terms r1 in [Kx g/G, Kx (g+1)/G) (its share of
+// the row stage and of the Kx Ky column steps; "shard r1") and the partial f
+// are summed once.  Non-fused plans run whole on the root (the others contribute zeros).
+int nufft_plan2d2_exec_multi(const nufft_plan2d* plan, const double* C_dev, double* f_dev, size_t batch,
+                             nufft_comm* comm, int root, int mode, void* stream) {
+    return guard([&] {
+        if (!plan || !comm) nb::throw_invalid("exec_multi: null argument");
+        if (mode != NUFFT_MULTI_REDUCE && mode != NUFFT_MULTI_ALLREDUCE) nb::throw_invalid("exec_multi: mode");
+        if (root < 0 || root >= comm->nranks) nb::throw_invalid("exec_multi: root out of range");
+        const nb::Plan2DState& st = plan->st;
+        if (st.device != comm->device) nb::throw_invalid("exec_multi: plan and communicator on different devices");
+        NB_CUDA(cudaSetDevice(st.device));
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+        nb::DevBuf part(sizeof(double2) * st.count * batch, s);
+        const double2* C = reinterpret_cast<const double2*>(C_dev);
+        if (st.fused) {
+            size_t r0, r1;
+            nb::term_range(st.kx, comm->nranks, comm->rank, &r0, &r1);
+            nb::exec_2d_fused(st, C, part.as<double2>(), batch, s, r0, r1);
+        } else if (comm->rank == root) {
+            nb::exec_2d(st, C, part.as<double2>(), batch, true, s);
+        } else {
+            NB_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double2) * st.count * batch, s));
+        }
+        const nb::NcclApi& api = nb::nccl();
+        if (mode == NUFFT_MULTI_ALLREDUCE)
+            nb::nccl_check(api.all_reduce(part.get(), f_dev, 2 * st.count * batch, ncclDouble, ncclSum, comm->comm, s),
+                           "ncclAllReduce");
+        else
+            nb::nccl_check(api.reduce(part.get(), f_dev, 2 * st.count * batch, ncclDouble, ncclSum, root, comm->comm, s),
+                           "ncclReduce");
+    });
+}
+
 int nufft_plan2_exec_terms_sorted(const nufft_plan2* plan, const double* c_dev, double* fs_dev, size_t r_begin,
                                   size_t r_end, void* stream) {
     return guard([&] {

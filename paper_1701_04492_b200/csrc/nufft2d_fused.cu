@@ -38,6 +38,20 @@ namespace {
 
 inline unsigned blocks(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// z (i h)^r0: the Horner-in-r1 sum of a partial term range [r0, r1hi) (multi-GPU r1 split)
+__device__ __forceinline__ double2 ipow_scale(double2 z, double h, int r0) {
+    if (r0 == 0) return z;
+    double hr = 1.0;
+    for (int m = 0; m < r0; ++m) hr *= h;
+    z = cscale(z, hr);
+    switch (r0 & 3) {
+        case 1: return make_double2(-z.y, z.x);
+        case 2: return make_double2(-z.x, -z.y);
+        case 3: return make_double2(z.y, -z.x);
+        default: return z;
+    }
+}
+
 constexpr int kQ2d = 20;  // samples per column-kernel thread (capacity 1.25 m per chunk)
 
 struct RowParams {
@@ -45,6 +59,7 @@ struct RowParams {
     int log_n;
     int kx;
     int ux_uniform;
+    int r1lo, r1hi;  // row-stage terms [r1lo, r1hi) (multi-GPU r1 split); R slice r1 - r1lo
 };
 
 struct ColParams {
@@ -61,6 +76,7 @@ struct ColParams {
     double2* A;         // sorted-order scratch
     int degx[kRankCap];
     int degy[kRankCap];
+    int r1lo, r1hi;     // r1 terms [r1lo, r1hi) of this launch; R slice r1 - r1lo
 };
 
 // ---------------------------------------------------------------- row stage
@@ -91,7 +107,18 @@ __global__ void __launch_bounds__(LN / 16, 1)
             tcur[q] = 0.5 * (two_s0 + 0.25 * q);
         }
         __syncthreads();
-        for (int r = 0; r < p.kx; ++r) {
+        for (int r = 0; r < p.r1hi; ++r) {
+            if (r < p.r1lo) {  // advance the recurrence to the first term of the range
+                if (r > 0) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const double tn = __fma_rn(two_s0 + 0.25 * q, tcur[q], -tprev[q]);
+                        tprev[q] = tcur[q];
+                        tcur[q] = tn;
+                    }
+                }
+                continue;
+            }
             if constexpr (FftShape<LN>::STAGES < 3) __syncthreads();
             double2 v[16];
 #pragma unroll
@@ -101,7 +128,7 @@ __global__ void __launch_bounds__(LN / 16, 1)
                 v[q] = make_double2(cv.x * vr, cv.y * vr);
             }
             block_fft<LN, -1>(v, buf0, buf1, tid, T, [] { __syncthreads(); });
-            double2* out = R + (long long)r * mn + ky * p.n;
+            double2* out = R + (long long)(r - p.r1lo) * mn + ky * p.n;
 #pragma unroll
             for (int q = 0; q < 16; ++q) out[tid + q * G] = v[q];
             if (r > 0) {
@@ -158,9 +185,9 @@ __global__ void __launch_bounds__(LM / 16, 1)
                 sty[i] = ok ? (unsigned short)(LM == 4096 ? fft2l_slot_of(p.tys[cb + i]) : p.tys[cb + i])
                             : (unsigned short)0;
             }
-            for (int r1 = p.kx - 1; r1 >= 0; --r1) {
+            for (int r1 = p.r1hi - 1; r1 >= p.r1lo; --r1) {
                 __syncthreads();  // previous term's gathers from buf / reads of rcol done
-                const double2* col = R + (long long)r1 * mn + tx;
+                const double2* col = R + (long long)(r1 - p.r1lo) * mn + tx;
 #pragma unroll
                 for (int q = 0; q < 16; ++q) rcol[tid + q * G] = __ldcs(col + (long long)(tid + q * G) * p.n);
                 double2 acc[Q];
@@ -230,14 +257,15 @@ __global__ void __launch_bounds__(LM / 16, 1)
                         for (int m = deg; m >= 0; --m) gx = __fma_rn(gx, w, a[m]);
                     }
                     double2 A = cscale(acc[u], gx);
-                    if (r1 != p.kx - 1) {
+                    if (r1 != p.r1hi - 1) {
                         const double2 prev = p.A[cb + i];
                         A.x = __fma_rn(-hx, prev.y, A.x);
                         A.y = __fma_rn(hx, prev.x, A.y);
                     }
-                    if (r1 > 0) {
+                    if (r1 > p.r1lo) {
                         p.A[cb + i] = A;
                     } else {
+                        A = ipow_scale(A, hx, p.r1lo);
                         double ph = 0.0, scale = 1.0;
                         if (!p.ux_uniform) {
                             ph += 2.0 * hx;
@@ -296,6 +324,7 @@ struct Col2Params {
     double2* A;         // sorted-order scratch
     int degx[kRankCap];
     int degy_top0, degy_top1;  // relative-accuracy degrees of gy_{Ky-1}, gy_{Ky}
+    int r1lo, r1hi;            // r1 terms [r1lo, r1hi) of this launch; R slice r1 - r1lo
 };
 
 __device__ __forceinline__ void c2_bar_sync(int id, int count) {
@@ -358,10 +387,10 @@ __global__ void __launch_bounds__(512, 1)
                 tm_stn<CH>(tl + W::COL_T + CH * k, sl);
             }
             tm_wait_st();
-            for (int r1 = p.kx - 1; r1 >= 0; --r1) {
+            for (int r1 = p.r1hi - 1; r1 >= p.r1lo; --r1) {
                 // block start: the R_r1 column (stride n) into shared memory; S = 0 and the
                 // gy pair (gy_{Ky-1}, gy_Ky) by the series, this group's chunks
-                const double2* col = R + (long long)r1 * mn + tx;
+                const double2* col = R + (long long)(r1 - p.r1lo) * mn + tx;
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     rcol[threadIdx.x + 512 * q] = __ldcg(col + (long long)(threadIdx.x + 512 * q) * p.n);
@@ -454,7 +483,7 @@ __global__ void __launch_bounds__(512, 1)
                     unsigned sv[4 * CH], hx[2 * CH], hy[2 * CH];
                     tm_ldn<4 * CH>(tl + W::COL_S + 4 * CH * k, sv);
                     tm_ldn<2 * CH>(tl + W::COL_HX + 2 * CH * k, hx);
-                    if (r1 == 0) tm_ldn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hy);
+                    if (r1 == p.r1lo) tm_ldn<2 * CH>(tl + W::COL_HY + 2 * CH * k, hy);
                     tm_wait_ld();
 #pragma unroll
                     for (int u = 0; u < CH; ++u) {
@@ -464,14 +493,15 @@ __global__ void __launch_bounds__(512, 1)
                         const double gx = p.ux_uniform ? 1.0 : bessel_g_rt(r1, dgx, h * h);
                         const double2 S = make_double2(mk64(sv[4 * u], sv[4 * u + 1]), mk64(sv[4 * u + 2], sv[4 * u + 3]));
                         double2 A = cscale(S, gx);
-                        if (r1 != p.kx - 1) {
+                        if (r1 != p.r1hi - 1) {
                             const double2 prev = p.A[cb + i];
                             A.x = __fma_rn(-h, prev.y, A.x);
                             A.y = __fma_rn(h, prev.x, A.y);
                         }
-                        if (r1 > 0) {
+                        if (r1 > p.r1lo) {
                             p.A[cb + i] = A;
                         } else {
+                            A = ipow_scale(A, h, p.r1lo);
                             const double hyv = mk64(hy[2 * u], hy[2 * u + 1]);
                             double sn, cs;
                             sincos(2.0 * (h + hyv), &sn, &cs);
@@ -541,10 +571,10 @@ int occupancy(const void* fn, int threads, size_t smem) {
 }
 
 template <int LN>
-void launch_rows(const double2* C, double2* R, const Plan2DState& st, cudaStream_t s) {
+void launch_rows(const double2* C, double2* R, const Plan2DState& st, cudaStream_t s, int r1lo, int r1hi) {
     const DeviceCtx& ctx = DeviceCtx::get(st.device);
     constexpr size_t SM = sizeof(double2) * (LN + 2 * padded_len(LN) + FftShapeX<LN>::TW_LEN);
-    RowParams p{(long long)st.m, (long long)st.n, ilog2(st.n), (int)st.kx, st.ux_uniform ? 1 : 0};
+    RowParams p{(long long)st.m, (long long)st.n, ilog2(st.n), (int)st.kx, st.ux_uniform ? 1 : 0, r1lo, r1hi};
     set_smem(k2d_rows<LN>, SM);
     const int grid = (int)std::min<long long>((long long)st.m,
                                               (long long)ctx.sms * occupancy((const void*)k2d_rows<LN>, LN / 16, SM));
@@ -552,7 +582,8 @@ void launch_rows(const double2* C, double2* R, const Plan2DState& st, cudaStream
     NB_LAUNCH();
 }
 
-void launch_cols_fs(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s) {
+void launch_cols_fs(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s, int r1lo,
+                    int r1hi) {
     const DeviceCtx& ctx = DeviceCtx::get(st.device);
     Col2Params p{};
     p.m = (long long)st.m;
@@ -568,6 +599,8 @@ void launch_cols_fs(const double2* R, double2* f, double2* A, const Plan2DState&
     p.coloff = st.fz.coloff.as<int>();
     p.vyt = st.fz.vyt.as<double>();
     p.A = A;
+    p.r1lo = r1lo;
+    p.r1hi = r1hi;
     for (size_t r = 0; r < st.deg_x.size() && r < (size_t)kRankCap; ++r) p.degx[r] = st.deg_x[r];
     p.degy_top0 = bessel_series_degree_rel(st.uy_uniform ? 0.0 : st.ay.gamma, (int)st.ky - 1);
     p.degy_top1 = bessel_series_degree_rel(st.uy_uniform ? 0.0 : st.ay.gamma, (int)st.ky);
@@ -578,8 +611,9 @@ void launch_cols_fs(const double2* R, double2* f, double2* A, const Plan2DState&
 }
 
 template <int LM>
-void launch_cols(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s) {
-    if constexpr (LM == 4096) return launch_cols_fs(R, f, A, st, s);
+void launch_cols(const double2* R, double2* f, double2* A, const Plan2DState& st, cudaStream_t s, int r1lo,
+                 int r1hi) {
+    if constexpr (LM == 4096) return launch_cols_fs(R, f, A, st, s, r1lo, r1hi);
     const DeviceCtx& ctx = DeviceCtx::get(st.device);
     constexpr size_t SM = ColShape<LM>::SMEM;
     ColParams p{};
@@ -597,6 +631,8 @@ void launch_cols(const double2* R, double2* f, double2* A, const Plan2DState& st
     p.coloff = st.fz.coloff.as<int>();
     p.vyt = st.fz.vyt.as<double>();
     p.A = A;
+    p.r1lo = r1lo;
+    p.r1hi = r1hi;
     for (size_t r = 0; r < st.deg_x.size() && r < (size_t)kRankCap; ++r) p.degx[r] = st.deg_x[r];
     for (size_t r = 0; r < st.deg_y.size() && r < (size_t)kRankCap; ++r) p.degy[r] = st.deg_y[r];
     set_smem(k2d_cols<LM>, SM);
@@ -663,15 +699,21 @@ void build_2d_fused(Plan2DState& st, cudaStream_t s) {
     st.fused = true;
 }
 
-void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s) {
+void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s, size_t r1_begin,
+                   size_t r1_end) {
     ensure_bessel_constants(st.device);
     const size_t mn = st.m * st.n;
-    DevBuf R(sizeof(double2) * mn * st.kx, s);
+    const int r1lo = (int)r1_begin, r1hi = (int)std::min(r1_end, st.kx);
+    if (r1hi <= r1lo) {
+        NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * st.count * batch, s));
+        return;
+    }
+    DevBuf R(sizeof(double2) * mn * (size_t)(r1hi - r1lo), s);
     DevBuf A(sizeof(double2) * std::max<size_t>(st.count, 1), s);
     const int LN = (int)st.n, LM = (int)st.m;
     for (size_t b = 0; b < batch; ++b) {
-        NB_SIZE_SWITCH(LN, launch_rows<LL>(C + b * mn, R.as<double2>(), st, s));
-        NB_SIZE_SWITCH(LM, launch_cols<LL>(R.as<double2>(), f + b * st.count, A.as<double2>(), st, s));
+        NB_SIZE_SWITCH(LN, launch_rows<LL>(C + b * mn, R.as<double2>(), st, s, r1lo, r1hi));
+        NB_SIZE_SWITCH(LM, launch_cols<LL>(R.as<double2>(), f + b * st.count, A.as<double2>(), st, s, r1lo, r1hi));
     }
 }
 

@@ -134,7 +134,8 @@ void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batc
 void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_t batch,
                           cudaStream_t s, cudaEvent_t* ev = nullptr, size_t r_begin = 0,
                           size_t r_end = SIZE_MAX);
-void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s);
+void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s,
+                size_t r_begin = 0, size_t r_end = SIZE_MAX);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,
              cudaStream_t s);
 
@@ -164,7 +165,8 @@ void nudft2d_direct(const double* x, const double* y, size_t cnt, const double2*
 
 bool fused_2d_eligible(size_t m, size_t n, size_t count);
 void build_2d_fused(Plan2DState& st, cudaStream_t s);
-void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s);
+void exec_2d_fused(const Plan2DState& st, const double2* C, double2* f, size_t batch, cudaStream_t s,
+                   size_t r1_begin = 0, size_t r1_end = SIZE_MAX);
 
 // elementwise helpers shared by the generic paths (generic_kernels.cu)
 void conj_copy(const double2* in, double2* out, size_t n, cudaStream_t s);

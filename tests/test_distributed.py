@@ -220,3 +220,71 @@ def test_type1_term_shards_and_single_rank_multi(nb, n):
     torch.cuda.synchronize()
     assert torch.equal(torch.view_as_real(got), torch.view_as_real(full))
     comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [4041, 4040])  # bTrivial; B made non-trivial below
+def test_type3_term_shards_and_single_rank_multi(nb, seed):
+    """Type-III outer-term split: partials over term ranges (inner transforms, beta dot
+    products, the epilogue's partial Horner sum times (ih)^r0) add up to the full
+    transform; exec_multi on a one-rank communicator equals exec."""
+    import torch
+    from paper_1701_04492_b200.parallel import NcclComm, unique_id
+    n = 1 << 16
+    rng = nb.GaussianSampler(seed)
+    x = rng.uniform_vector(n, 0.0, 1.0)
+    if seed == 4040:
+        x[7] = 1.0 - 0.25 / n  # a sample on the node at 1: B non-trivial
+    w = rng.uniform_vector(n, 0.0, float(n))
+    p = nb.plan_nufft3(x, w, 1e-9, device=0)
+    assert p.bTrivial == (seed == 4041)
+    c = torch.from_numpy(rng.complex_vector(n)).cuda()
+    full = torch.empty_like(c)
+    p.execute_device(c.data_ptr(), full.data_ptr())
+    K = p.rank_a
+    acc = torch.zeros_like(c)
+    for g in range(3):
+        r0, r1 = term_range(K, 3, g)
+        part = torch.empty_like(c)
+        p.execute_terms_device(c.data_ptr(), part.data_ptr(), r0, r1)
+        acc += part
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(acc - full) / torch.linalg.norm(full)).item() <= 1e-14
+    comm = NcclComm(unique_id(), 1, 0, 0)
+    got = torch.full_like(c, float("nan"))
+    p.execute_multi_device(c.data_ptr(), got.data_ptr(), comm)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(full))
+    comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(4096, 64), (256, 512), (64, 16)])
+def test_2d_r1_shards_and_single_rank_multi(nb, m, n):
+    """2D r1 split (row-stage terms): partials over r1 ranges add up to the full transform
+    (both column kernels: m = 4096 two-group, others single-group), exec_multi on a one-rank
+    communicator equals exec."""
+    import torch
+    from paper_1701_04492_b200.parallel import NcclComm, unique_id
+    cnt = 3 * m * n // 4 + 5
+    rng = nb.GaussianSampler(m + n)
+    p = nb.plan_nufft2d2(rng.uniform_vector(cnt, 0.0, 1.0), rng.uniform_vector(cnt, 0.0, 1.0), m, n, 1e-9, device=0)
+    assert p.fused
+    C = torch.from_numpy(rng.complex_vector(m * n)).cuda()
+    full = torch.empty(cnt, dtype=torch.complex128, device="cuda")
+    p.execute_device(C.data_ptr(), full.data_ptr())
+    K = p.rank_x()
+    acc = torch.zeros_like(full)
+    for g in range(3):
+        r0, r1 = term_range(K, 3, g)
+        part = torch.empty_like(full)
+        p.execute_terms_device(C.data_ptr(), part.data_ptr(), r0, r1)
+        acc += part
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(acc - full) / torch.linalg.norm(full)).item() <= 1e-14
+    comm = NcclComm(unique_id(), 1, 0, 0)
+    got = torch.full_like(full, float("nan"))
+    p.execute_multi_device(C.data_ptr(), got.data_ptr(), comm)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(full))
+    comm.close()
