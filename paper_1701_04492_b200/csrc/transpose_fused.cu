@@ -325,67 +325,83 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
             for (int r = p.r0; r < p.r1; ++r) {
                 if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 gsync();  // previous term's last-stage reads of buf (and the TMA's) are done
-                // term phase: buf[i] = g_r(h_i^2) Q_i, then Q_i <- h_i Q_i
+                // term phase: buf[i] = g_r(h_i^2) Q_i, then Q_i <- h_i Q_i.  Two TMEM chunks
+                // (8 samples) share one Horner loop (8 independent FMA chains per coefficient)
                 const double* a = kBes + r * kSeriesTerms;
                 const int deg = p.deg[r];
+                constexpr int NCHK = (QA + 3) / 4;
 #pragma unroll
-                for (int k = 0; k < (QA + 3) / 4; ++k) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
-                    const bool full = 4 * k + 4 <= QA;
-                    unsigned qv[16], hv[8];
-                    if (full) {
-                        tm_ld16(tcol + S::COL_Q + 16 * k, qv);
-                        tm_ld8(tcol + S::COL_H + 8 * k, hv);
-                    } else {
-                        tm_ld4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
-                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
-                                     : "=r"(hv[0]), "=r"(hv[1])
-                                     : "r"(tcol + S::COL_H + 8 * k)
-                                     : "memory");
+                for (int k0 = 0; k0 < NCHK; k0 += 2) {
+                    double h[8], w[8], gr[8];
 #pragma unroll
-                        for (int c = 4; c < 16; ++c) qv[c] = 0u;
+                    for (int c = 0; c < 2; ++c) {
+                        const int k = k0 + c;
+                        unsigned hv[8];
 #pragma unroll
-                        for (int c = 2; c < 8; ++c) hv[c] = 0u;
-                    }
-                    tm_wait_ld();
-                    double h[4], w[4], gr[4];
+                        for (int e = 0; e < 8; ++e) hv[e] = 0u;
+                        if (k < NCHK) {
+                            if (4 * k + 4 <= QA) {
+                                tm_ld8(tcol + S::COL_H + 8 * k, hv);
+                            } else {
+                                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                                             : "=r"(hv[0]), "=r"(hv[1])
+                                             : "r"(tcol + S::COL_H + 8 * k)
+                                             : "memory");
+                            }
+                        }
+                        tm_wait_ld();
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        h[u] = mk64(hv[2 * u], hv[2 * u + 1]);
-                        w[u] = h[u] * h[u];
+                        for (int u = 0; u < 4; ++u) {
+                            h[4 * c + u] = mk64(hv[2 * u], hv[2 * u + 1]);
+                            w[4 * c + u] = h[4 * c + u] * h[4 * c + u];
+                        }
                     }
                     if constexpr (UNIFORM) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) gr[u] = 1.0;
+                        for (int u = 0; u < 8; ++u) gr[u] = 1.0;
                     } else {
                         // rolled Horner (uniform degree; the same operations as series_fixed):
                         // the switch-unrolled form multiplied the kernel's code size
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) gr[u] = a[deg];
+                        for (int u = 0; u < 8; ++u) gr[u] = a[deg];
 #pragma unroll 1
                         for (int m = deg - 1; m >= 0; --m) {
                             const double am = a[m];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
+                            for (int u = 0; u < 8; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int uu = 4 * k + u;
-                        if (uu >= QA) break;
-                        const double2 Qv =
-                            make_double2(mk64(qv[4 * u], qv[4 * u + 1]), mk64(qv[4 * u + 2], qv[4 * u + 3]));
-                        buf[tid + uu * G] = cscale(Qv, gr[u]);
-                        const double2 Qn = UNIFORM ? Qv : cscale(Qv, h[u]);
-                        qv[4 * u] = lo32(Qn.x);
-                        qv[4 * u + 1] = hi32(Qn.x);
-                        qv[4 * u + 2] = lo32(Qn.y);
-                        qv[4 * u + 3] = hi32(Qn.y);
-                    }
-                    if constexpr (!UNIFORM) {
-                        if (full) tm_st16(tcol + S::COL_Q + 16 * k, qv);
-                        else tm_st4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                    for (int c = 0; c < 2; ++c) {
+                        const int k = k0 + c;
+                        if (k >= NCHK) break;
+                        const bool full = 4 * k + 4 <= QA;
+                        unsigned qv[16];
+                        if (full) {
+                            tm_ld16(tcol + S::COL_Q + 16 * k, qv);
+                        } else {
+                            tm_ld4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+#pragma unroll
+                            for (int e = 4; e < 16; ++e) qv[e] = 0u;
+                        }
+                        tm_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int uu = 4 * k + u;
+                            if (uu >= QA) break;
+                            const double2 Qv =
+                                make_double2(mk64(qv[4 * u], qv[4 * u + 1]), mk64(qv[4 * u + 2], qv[4 * u + 3]));
+                            buf[tid + uu * G] = cscale(Qv, gr[4 * c + u]);
+                            const double2 Qn = UNIFORM ? Qv : cscale(Qv, h[4 * c + u]);
+                            qv[4 * u] = lo32(Qn.x);
+                            qv[4 * u + 1] = hi32(Qn.x);
+                            qv[4 * u + 2] = lo32(Qn.y);
+                            qv[4 * u + 3] = hi32(Qn.y);
+                        }
+                        if constexpr (!UNIFORM) {
+                            if (full) tm_st16(tcol + S::COL_Q + 16 * k, qv);
+                            else tm_st4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                        }
                     }
                 }
                 gsync();  // terms visible
