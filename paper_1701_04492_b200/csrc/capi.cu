@@ -535,10 +535,14 @@ int nufft_plan2_exec_host(const nufft_plan2* plan, const double* c, size_t len, 
     });
 }
 static void adjoint_dev(const nb::CorePlan& p, const double2* fin, double2* out, cudaStream_t s) {
-    nb::DevBuf g(16 * p.n, s);
-    nb::conj_copy(fin, g.as<double2>(), p.n, s);
-    nb::exec_transpose(p, g.as<double2>(), out, 1, s);
-    nb::conj_copy(out, out, p.n, s);
+    if (p.fused) {  // conj(F2~^T conj(f)) with the conjugations folded into the transpose core
+        nb::exec_transpose_fused(p, fin, out, 1, s, nullptr, 0, p.K, /*conj=*/true);
+    } else {
+        nb::DevBuf g(16 * p.n, s);
+        nb::conj_copy(fin, g.as<double2>(), p.n, s);
+        nb::exec_transpose(p, g.as<double2>(), out, 1, s);
+        nb::conj_copy(out, out, p.n, s);
+    }
     nb::fft_count(p.n, p.K);
 }
 int nufft_plan2_adjoint(const nufft_plan2* plan, const double* f_dev, double* out_dev, void* stream) {

@@ -131,9 +131,10 @@ void exec_transpose(const CorePlan& p, const double2* g, double2* f, size_t batc
                     cudaStream_t s, size_t r_begin = 0, size_t r_end = SIZE_MAX);
 // fused two-pass form of exec_transpose for power-of-two N (transpose_fused.cu);
 // ev as for exec_type2
+// conj: transform conj(g) and write conj(f) (the adjoints, with no separate conjugation passes)
 void exec_transpose_fused(const CorePlan& p, const double2* g, double2* f, size_t batch,
                           cudaStream_t s, cudaEvent_t* ev = nullptr, size_t r_begin = 0,
-                          size_t r_end = SIZE_MAX);
+                          size_t r_end = SIZE_MAX, bool conj = false);
 void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch, cudaStream_t s,
                 size_t r_begin = 0, size_t r_end = SIZE_MAX);
 void exec_2d(const Plan2DState& p, const double2* C, double2* f, size_t batch, bool reuse_rows,

@@ -51,12 +51,14 @@ struct PassAParams {
     const int* perm;
     const int* rowoff;
     int deg[kRankCap];
+    int conj;  // transform conj(g) (the adjoints: F2~* f = conj(F2~^T conj(f)), transforms.hpp:226-232)
 };
 
 struct PassBParams {
     long long n;
     int log_n1, log_n2;
     int r0, r1;
+    int conj;  // write conj(f)
 };
 
 // multiply by i^r
@@ -124,7 +126,8 @@ __global__ void __launch_bounds__(L2 / 16, 1)
                 const unsigned t2 = p.skey[cb + i] & mask;
                 if (i == 0 || (p.skey[cb + i - 1] & mask) != t2) bo16[2 * t2] = (unsigned short)i;
                 if (i == cnt - 1 || (p.skey[cb + i + 1] & mask) != t2) bo16[2 * t2 + 1] = (unsigned short)(i + 1);
-                const double2 gv = __ldg(g + p.perm[cb + i]);
+                double2 gv = __ldg(g + p.perm[cb + i]);
+                if (p.conj) gv.y = -gv.y;
                 if constexpr (UNIFORM) {
                     gs[i] = gv;
                 } else {
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                     double h = 0.0;
                     if (uu < QA && i < cnt) {
                         Gj = __ldg(g + p.perm[cb + i]);
+                        if (p.conj) Gj.y = -Gj.y;
                         if constexpr (!UNIFORM) {
                             h = half_phase(p.ds[cb + i]);
                             double sn, cs;
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(L1 / 16, 1)
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const long long k1 = tid + q * G;
-            f[(k1 << p.log_n2) + k2] = acc[q];
+            f[(k1 << p.log_n2) + k2] = p.conj ? cconj(acc[q]) : acc[q];
         }
     }
 }
@@ -734,8 +738,8 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const long long k1 = k1_0 + (4 * j + u) * G;
-                f[(k1 << p.log_n2) + k2] =
-                    make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+                const double2 fv = make_double2(mk64(av[4 * u], av[4 * u + 1]), mk64(av[4 * u + 2], av[4 * u + 3]));
+                f[(k1 << p.log_n2) + k2] = p.conj ? cconj(fv) : fv;
             }
         }
     }
@@ -746,7 +750,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
 
 // N1 == 1: f[k] = sum_r v_r(k) Z_r[k]
 __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ f, long long N,
-                           int r0, int r1, int uniform) {
+                           int r0, int r1, int uniform, int conj) {
     const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= N) return;
     const double s = __dsub_rn(__dmul_rn(2.0, (double)k / (double)N), 1.0);
@@ -773,7 +777,7 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
             acc.y = __fma_rn(vr, z.y, acc.y);
         }
     }
-    f[k] = acc;
+    f[k] = conj ? cconj(acc) : acc;
 }
 
 // Z columns (rr*N + t1*4096 + k2, N1 = 2^log_n1 rows) as the 5-D tensor k1_passB_tm<.., TMA>
@@ -831,10 +835,11 @@ int occupancy(const void* fn, int threads, size_t smem) {
 }
 
 template <int L2>
-void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     constexpr size_t SM = PassAShape<L2>::SMEM;
     PassAParams p{};
+    p.conj = conj ? 1 : 0;
     p.n = (long long)pl.n;
     p.log_n1 = pl.bk.log_n1;
     p.log_n2 = pl.bk.log_n2;
@@ -883,11 +888,11 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
 }
 
 template <int L1>
-void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     if constexpr (L1 >= 2048) {
         size_t SMT = sizeof(double2) * (2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN);
-        PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+        PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1, conj ? 1 : 0};
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
         CUtensorMap zmap{};
         if constexpr (L1 == 4096) {
@@ -906,7 +911,7 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         return;
     }
     constexpr size_t SM = sizeof(double2) * (2 * padded_len(L1) + 16 + FftShapeX<L1>::TW_LEN);
-    PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1};
+    PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1, conj ? 1 : 0};
     auto fn = pl.uniform ? k1_passB<L1, true> : k1_passB<L1, false>;
     set_smem(fn, SM);
     const long long n2 = 1ll << pl.bk.log_n2;
@@ -915,32 +920,32 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
     NB_LAUNCH();
 }
 
-void dispatch_passA(int L, const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+void dispatch_passA(int L, const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
     switch (L) {
-        case 16: return launch_passA<16>(g, Z, pl, r0, r1, s);
-        case 32: return launch_passA<32>(g, Z, pl, r0, r1, s);
-        case 64: return launch_passA<64>(g, Z, pl, r0, r1, s);
-        case 128: return launch_passA<128>(g, Z, pl, r0, r1, s);
-        case 256: return launch_passA<256>(g, Z, pl, r0, r1, s);
-        case 512: return launch_passA<512>(g, Z, pl, r0, r1, s);
-        case 1024: return launch_passA<1024>(g, Z, pl, r0, r1, s);
-        case 2048: return launch_passA<2048>(g, Z, pl, r0, r1, s);
-        case 4096: return launch_passA<4096>(g, Z, pl, r0, r1, s);
+        case 16: return launch_passA<16>(g, Z, pl, r0, r1, conj, s);
+        case 32: return launch_passA<32>(g, Z, pl, r0, r1, conj, s);
+        case 64: return launch_passA<64>(g, Z, pl, r0, r1, conj, s);
+        case 128: return launch_passA<128>(g, Z, pl, r0, r1, conj, s);
+        case 256: return launch_passA<256>(g, Z, pl, r0, r1, conj, s);
+        case 512: return launch_passA<512>(g, Z, pl, r0, r1, conj, s);
+        case 1024: return launch_passA<1024>(g, Z, pl, r0, r1, conj, s);
+        case 2048: return launch_passA<2048>(g, Z, pl, r0, r1, conj, s);
+        case 4096: return launch_passA<4096>(g, Z, pl, r0, r1, conj, s);
         default: throw Error(kInternal, "pass A size");
     }
 }
 
-void dispatch_passB(int L, const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, cudaStream_t s) {
+void dispatch_passB(int L, const double2* Z, double2* f, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
     switch (L) {
-        case 16: return launch_passB<16>(Z, f, pl, r0, r1, s);
-        case 32: return launch_passB<32>(Z, f, pl, r0, r1, s);
-        case 64: return launch_passB<64>(Z, f, pl, r0, r1, s);
-        case 128: return launch_passB<128>(Z, f, pl, r0, r1, s);
-        case 256: return launch_passB<256>(Z, f, pl, r0, r1, s);
-        case 512: return launch_passB<512>(Z, f, pl, r0, r1, s);
-        case 1024: return launch_passB<1024>(Z, f, pl, r0, r1, s);
-        case 2048: return launch_passB<2048>(Z, f, pl, r0, r1, s);
-        case 4096: return launch_passB<4096>(Z, f, pl, r0, r1, s);
+        case 16: return launch_passB<16>(Z, f, pl, r0, r1, conj, s);
+        case 32: return launch_passB<32>(Z, f, pl, r0, r1, conj, s);
+        case 64: return launch_passB<64>(Z, f, pl, r0, r1, conj, s);
+        case 128: return launch_passB<128>(Z, f, pl, r0, r1, conj, s);
+        case 256: return launch_passB<256>(Z, f, pl, r0, r1, conj, s);
+        case 512: return launch_passB<512>(Z, f, pl, r0, r1, conj, s);
+        case 1024: return launch_passB<1024>(Z, f, pl, r0, r1, conj, s);
+        case 2048: return launch_passB<2048>(Z, f, pl, r0, r1, conj, s);
+        case 4096: return launch_passB<4096>(Z, f, pl, r0, r1, conj, s);
         default: throw Error(kInternal, "pass B size");
     }
 }
@@ -948,7 +953,7 @@ void dispatch_passB(int L, const double2* Z, double2* f, const CorePlan& pl, int
 }  // namespace
 
 void exec_transpose_fused(const CorePlan& pl, const double2* g, double2* f, size_t batch,
-                          cudaStream_t s, cudaEvent_t* ev, size_t r_begin, size_t r_end) {
+                          cudaStream_t s, cudaEvent_t* ev, size_t r_begin, size_t r_end, bool conj) {
     ensure_bessel_constants(pl.device);
     const size_t N = pl.n;
     const int r0 = (int)r_begin, r1 = (int)std::min(r_end, pl.K);
@@ -960,14 +965,14 @@ void exec_transpose_fused(const CorePlan& pl, const double2* g, double2* f, size
     const int L1 = 1 << pl.bk.log_n1, L2 = 1 << pl.bk.log_n2;
     for (size_t b = 0; b < batch; ++b) {
         if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[0], s));
-        dispatch_passA(L2, g + b * N, Z.as<double2>(), pl, r0, r1, s);
+        dispatch_passA(L2, g + b * N, Z.as<double2>(), pl, r0, r1, conj, s);
         if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[1], s));
         if (pl.bk.log_n1 == 0) {
             k1_combine<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(Z.as<double2>(), f + b * N, (long long)N,
-                                                                 r0, r1, pl.uniform ? 1 : 0);
+                                                                 r0, r1, pl.uniform ? 1 : 0, conj ? 1 : 0);
             NB_LAUNCH();
         } else {
-            dispatch_passB(L1, Z.as<double2>(), f + b * N, pl, r0, r1, s);
+            dispatch_passB(L1, Z.as<double2>(), f + b * N, pl, r0, r1, conj, s);
         }
         if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[2], s));
     }
