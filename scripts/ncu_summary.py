@@ -5,7 +5,7 @@
   * profiles/ncu_traffic.json  (DRAM read+write bytes per launch, the bench's roofline.traffic),
   * profiles/fp64.json         (FP64 thread-instructions per launch and the measured DFMA peak,
                                 the bench's roofline.fp64).
-Usage: ncu_summary.py REP OUT_TXT [n] [K]"""
+Usage: ncu_summary.py REP OUT_TXT [n] [K] [--no-json]   (--no-json: text summary only)"""
 import csv
 import json
 import os
@@ -13,9 +13,11 @@ import subprocess
 import sys
 from collections import defaultdict
 
-rep, out_txt = sys.argv[1], sys.argv[2]
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 24
-K = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+write_json = "--no-json" not in sys.argv
+argv = [a for a in sys.argv if a != "--no-json"]
+rep, out_txt = argv[1], argv[2]
+n = int(argv[3]) if len(argv) > 3 else 1 << 24
+K = int(argv[4]) if len(argv) > 4 else 20
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
@@ -93,6 +95,8 @@ for name, ds in per.items():
     lines += ["    " + ln for ln in hot.splitlines()[1:]]
 open(out_txt, "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
+if not write_json:
+    sys.exit(0)
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 peak_file = os.path.join(ROOT, "profiles", "r2_microbench_pipes.txt")
 per_clk, clk = 63.37, 1.965e9
