@@ -372,11 +372,46 @@ __device__ __forceinline__ int fft2l_slot(int tid, int b) {
 struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
-template <int SIGN, class Bar, class PreWrite = NoHook>
+// a[t] *= pre * w^t (t = 0..15): apply_pow_twiddles<16> with a thread-constant
+// factor pre folded into the generated powers (pre * w^t = (pre * w^(t - 2^e)) * w^(2^e)):
+// 15 products to form the factors instead of 11, 16 applications instead of 15 —
+// cheaper than scaling the 16 inputs of the DFT by pre separately.
+template <int SIGN>
+__device__ __forceinline__ void apply_pow_twiddles_pre(double2* a, const double2* bs, double2 pre) {
+    const double2 p1 = tw_sign<SIGN>(bs[0]), p2 = tw_sign<SIGN>(bs[256]);
+    const double2 p4 = tw_sign<SIGN>(bs[512]), p8 = tw_sign<SIGN>(bs[768]);
+    const double2 q1 = cmul(pre, p1), q2 = cmul(pre, p2), q3 = cmul(q1, p2);
+    const double2 q4 = cmul(pre, p4), q5 = cmul(q1, p4), q6 = cmul(q2, p4), q7 = cmul(q3, p4);
+    a[0] = cmul(a[0], pre);
+    a[1] = cmul(a[1], q1);
+    a[2] = cmul(a[2], q2);
+    a[3] = cmul(a[3], q3);
+    a[4] = cmul(a[4], q4);
+    a[5] = cmul(a[5], q5);
+    a[6] = cmul(a[6], q6);
+    a[7] = cmul(a[7], q7);
+    a[8] = cmul(a[8], cmul(pre, p8));
+    a[9] = cmul(a[9], cmul(q1, p8));
+    a[10] = cmul(a[10], cmul(q2, p8));
+    a[11] = cmul(a[11], cmul(q3, p8));
+    a[12] = cmul(a[12], cmul(q4, p8));
+    a[13] = cmul(a[13], cmul(q5, p8));
+    a[14] = cmul(a[14], cmul(q6, p8));
+    a[15] = cmul(a[15], cmul(q7, p8));
+}
+
+// PRE: the 16 inputs of the thread carry a common factor `pre` that is applied
+// with the first-level twiddles instead (the first-level DFT is linear).
+template <int SIGN, bool PRE = false, class Bar, class PreWrite = NoHook>
 __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
-                                             Bar bar, PreWrite pre_write = PreWrite()) {
+                                             Bar bar, PreWrite pre_write = PreWrite(),
+                                             double2 pre = make_double2(1.0, 0.0)) {
     dft<16, SIGN>(v);
-    apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
+    if constexpr (PRE) {
+        apply_pow_twiddles_pre<SIGN>(v, T.tb + tid, pre);
+    } else {
+        apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
+    }
     pre_write();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 256 + (tid ^ fft2l_swz(k1))] = v[k1];

@@ -300,10 +300,12 @@ __global__ void __launch_bounds__(512, 1)
     const int tid = threadIdx.x - grp * G;
     double2* buf = smem + grp * padded_len(L1);
     double2* step = smem + 2 * padded_len(L1) + grp * 16;
-    double2* tw = smem + 2 * padded_len(L1) + 32;
-    twiddle_table_build<L1>(tw, threadIdx.x, 2 * G);
+    // per-column FFT twiddles with the inter-pass twiddle folded in (see below)
+    double2* tbw = smem + 2 * padded_len(L1) + 32 + grp * 1024;        // [e][tid]
+    double2* t16c = smem + 2 * padded_len(L1) + 32 + 2048 + grp * 256;  // [a][u]
     Twiddles<L1> T;
-    twiddle_init<L1>(T, tw, tid);
+    T.tb = tbw;
+    T.t16 = t16c;
     if (threadIdx.x < 32) tm_alloc(&tmem_base, 512u);
     tm_fence_before();
     __syncthreads();
@@ -318,10 +320,24 @@ __global__ void __launch_bounds__(512, 1)
     double2* stg = buf + ((warp * 16 + u) * 2 + e);  // + 256 b: staging slot of output b
     const unsigned buf_s = (unsigned)__cvta_generic_to_shared(buf);
     for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
-        gsync();  // previous column's readers of step are done
+        gsync();  // previous column's readers of step / t16c are done
+        // The inter-pass twiddle w_N^{k2 t1} of output t1 = g + 16 a + 256 b of the
+        // two-level FFT (block_fft_2l) splits as w_N^{k2 g} w_N^{16 k2 a} w_N^{256 k2 b}:
+        //  * g is the first-level output index k1: w_N^{k2 k1} joins the first-level
+        //    twiddle w_4096^{tid k1} = w_N^{N2 tid k1}, i.e. the power bases become
+        //    w_N^{(N2 tid + k2) 2^e} (thread-private entries, no barrier needed);
+        //  * a is the second-level twiddle index: w_256^{u a} w_N^{16 k2 a} = t16c[a][u];
+        //  * b is the last DFT's output index: step[b] = w_N^{256 k2 b}, applied below.
+        // 15 complex products per thread and term instead of 32 (base * step[b], then
+        // times the value); every factor comes from one correctly rounded sincospi.
         for (int q = tid; q < 16; q += G) step[q] = unit_root(k2 * q * G, N);  // w_N^{k2 q G}
-        const int t1_0 = fft2l_out_index(tid, 0);
-        const double2 base = unit_root(k2 * t1_0, N);  // w_N^{k2 t1_0}
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            tbw[e * 256 + tid] = unit_root(((((long long)tid << p.log_n2) + k2) << e) & (N - 1), N);
+        {
+            const long long a = tid >> 4, uu = tid & 15;
+            t16c[tid] = unit_root(((uu * (N >> 8) + 16 * k2) * a) & (N - 1), N);
+        }
         const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -386,7 +402,7 @@ __global__ void __launch_bounds__(512, 1)
             });
             gsync();  // exchange reads done: buf becomes the staging box
 #pragma unroll
-            for (int b = 0; b < 16; ++b) stg[256 * b] = cmul(v[b], cmul(base, step[b]));
+            for (int b = 0; b < 16; ++b) stg[256 * b] = b == 0 ? v[0] : cmul(v[b], step[b]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             gsync();  // box complete
             if (tid == 0) {
@@ -1403,8 +1419,9 @@ void launch_pass1(const double2* c, double2* Y, const CorePlan& pl, int r0, int 
                 CUtensorMap map;
                 if (!make_y_tensor_map(&map, Y, pl.bk.log_n2, r1 - r0))
                     throw Error(kCudaError, "cuTensorMapEncodeTiled failed for the pass-1 Y map");
-                set_smem(k2_pass1_tma, SMT);
-                k2_pass1_tma<<<grid, 512, SMT, s>>>(c, map, p);
+                constexpr size_t SMA = sizeof(double2) * (2 * padded_len(4096) + 32 + 2048 + 512);
+                set_smem(k2_pass1_tma, SMA);
+                k2_pass1_tma<<<grid, 512, SMA, s>>>(c, map, p);
                 NB_LAUNCH();
                 return;
             }

@@ -664,11 +664,11 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             if constexpr (TMA) {
                 col_wait(bar_s0, col_phase);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[q] = cmul(pre[tid + q * G], cmul(base, step[q]));
+                for (int q = 0; q < 8; ++q) v[q] = q == 0 ? pre[tid] : cmul(pre[tid + q * G], step[q]);
                 col_wait(bar_s1, col_phase);
                 col_phase ^= 1;
 #pragma unroll
-                for (int q = 8; q < 16; ++q) v[q] = cmul(buf[tid + (q - 8) * G], cmul(base, step[q]));
+                for (int q = 8; q < 16; ++q) v[q] = cmul(buf[tid + (q - 8) * G], step[q]);
             } else {
                 const double2* col = Z + (long long)(r - p.r0) * N + k2;
 #pragma unroll
@@ -681,7 +681,11 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             if constexpr (TMA) {
                 if (tid == 0 && r + 1 < p.r1) col_load(0, r + 1 - p.r0, k2);  // pre is free: a whole term ahead
             }
-            if constexpr (F2L) {
+            if constexpr (TMA) {
+                // the inter-pass twiddle w_N^{k2 (tid + 256 q)} = base * step[q]: step[q] on
+                // the inputs above, the thread constant base with the first-level twiddles
+                block_fft_2l<-1, true>(v, buf, tid, T, gsync, NoHook(), base);
+            } else if constexpr (F2L) {
                 block_fft_2l<-1>(v, buf, tid, T, gsync);
             } else {
                 block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
