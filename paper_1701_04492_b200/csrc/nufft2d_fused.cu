@@ -522,20 +522,25 @@ __global__ void __launch_bounds__(512, 1)
     if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);
 }
 
-__global__ void k2d_keys(const long long* __restrict__ tx, long long count, unsigned* __restrict__ keys,
-                         int* __restrict__ idx) {
+// sort key (tx, ty): samples of a column in ascending ty, so the X[ty] gathers of a
+// warp (consecutive sorted samples) hit consecutive slots of the FFT buffer — spread
+// over all banks by the fft2l swizzle — instead of random ones (about half the
+// shared-memory wavefronts per gather).  The order inside a column does not change
+// any result: every sample keeps its own accumulators.
+__global__ void k2d_keys(const long long* __restrict__ tx, const long long* __restrict__ ty, int log_m,
+                         long long count, unsigned* __restrict__ keys, int* __restrict__ idx) {
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= count) return;
-    keys[j] = (unsigned)tx[j];
+    keys[j] = ((unsigned)tx[j] << log_m) | (unsigned)ty[j];
     idx[j] = (int)j;
 }
 
-__global__ void k2d_offsets(const unsigned* __restrict__ keys, long long count, long long nb,
+__global__ void k2d_offsets(const unsigned* __restrict__ keys, int log_m, long long count, long long nb,
                             int* __restrict__ off) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i > count) return;
-    const long long cur = (i < count) ? (long long)keys[i] : nb;
-    const long long prev = (i > 0) ? (long long)keys[i - 1] : -1;
+    const long long cur = (i < count) ? (long long)(keys[i] >> log_m) : nb;
+    const long long prev = (i > 0) ? (long long)(keys[i - 1] >> log_m) : -1;
     for (long long b = prev + 1; b <= cur; ++b) off[b] = (int)i;
 }
 
@@ -670,10 +675,11 @@ void build_2d_fused(Plan2DState& st, cudaStream_t s) {
     const size_t count = st.count, n = st.n, m = st.m;
     DevBuf keys(4 * count, s), keys_out(4 * count, s), idx(4 * count, s);
     st.fz.perm.alloc(4 * count);
-    k2d_keys<<<blocks(count), 256, 0, s>>>(st.ax.t.as<long long>(), (long long)count, keys.as<unsigned>(),
-                                          idx.as<int>());
+    const int log_m = ilog2(m);
+    k2d_keys<<<blocks(count), 256, 0, s>>>(st.ax.t.as<long long>(), st.ay.t.as<long long>(), log_m,
+                                          (long long)count, keys.as<unsigned>(), idx.as<int>());
     NB_LAUNCH();
-    const int bits = std::max(1, ilog2(n));
+    const int bits = std::max(1, ilog2(n) + log_m);
     size_t temp = 0;
     NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
                                             idx.as<int>(), st.fz.perm.as<int>(), (int)count, 0, bits, s));
@@ -681,7 +687,7 @@ void build_2d_fused(Plan2DState& st, cudaStream_t s) {
     NB_CUDA(cub::DeviceRadixSort::SortPairs(tb.get(), temp, keys.as<unsigned>(), keys_out.as<unsigned>(),
                                             idx.as<int>(), st.fz.perm.as<int>(), (int)count, 0, bits, s));
     st.fz.coloff.alloc(4 * (n + 1));
-    k2d_offsets<<<blocks(count + 1), 256, 0, s>>>(keys_out.as<unsigned>(), (long long)count, (long long)n,
+    k2d_offsets<<<blocks(count + 1), 256, 0, s>>>(keys_out.as<unsigned>(), log_m, (long long)count, (long long)n,
                                                  st.fz.coloff.as<int>());
     NB_LAUNCH();
     st.fz.dxs.alloc(8 * count);
