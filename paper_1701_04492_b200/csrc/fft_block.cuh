@@ -366,6 +366,27 @@ __device__ __forceinline__ int fft2l_slot(int tid, int b) {
     return g * 256 + 16 * u + (b ^ fft2l_swz(g) ^ (u & 7));
 }
 
+// a[t] *= p1^t (t = 1..15) given p1, p2 = p1^2, p4, p8 in registers
+__device__ __forceinline__ void apply_pow_twiddles_regs(double2* a, double2 p1, double2 p2, double2 p4, double2 p8) {
+    const double2 p3 = cmul(p1, p2);
+    a[1] = cmul(a[1], p1);
+    a[2] = cmul(a[2], p2);
+    a[3] = cmul(a[3], p3);
+    const double2 p5 = cmul(p1, p4), p6 = cmul(p2, p4), p7 = cmul(p3, p4);
+    a[4] = cmul(a[4], p4);
+    a[5] = cmul(a[5], p5);
+    a[6] = cmul(a[6], p6);
+    a[7] = cmul(a[7], p7);
+    a[8] = cmul(a[8], p8);
+    a[9] = cmul(a[9], cmul(p1, p8));
+    a[10] = cmul(a[10], cmul(p2, p8));
+    a[11] = cmul(a[11], cmul(p3, p8));
+    a[12] = cmul(a[12], cmul(p4, p8));
+    a[13] = cmul(a[13], cmul(p5, p8));
+    a[14] = cmul(a[14], cmul(p6, p8));
+    a[15] = cmul(a[15], cmul(p7, p8));
+}
+
 // PreWrite: called once, after the first-level DFT and twiddles and before the
 // first write to buf — the point by which buf must be free (callers whose
 // buf is still being read by the TMA engine wait there, not before the FFT).
@@ -402,7 +423,16 @@ __device__ __forceinline__ void apply_pow_twiddles_pre(double2* a, const double2
 
 // PRE: the 16 inputs of the thread carry a common factor `pre` that is applied
 // with the first-level twiddles instead (the first-level DFT is linear).
-template <int SIGN, bool PRE = false, class Bar, class PreWrite = NoHook>
+// TW2: how the second-level twiddles w^{u a} reach the registers —
+//   0: 15 loads from the [a][u] table t16 after the second DFT;
+//   1: the four bases (rows a = 1, 2, 4, 8 of t16) loaded after the exchange reads, powers generated
+//      (11 more complex products per thread);
+//   2: the same bases loaded ahead of the exchange (16 registers carried across it).
+// Table loads issued between the second DFT and the transpose queue behind the other worker's
+// exchange traffic in the shared-memory pipe: 3997 (0) / 3800 (1) / 3650 (2) cycles per FFT per SM
+// with two free-running workers (scripts/microbench_fft9.cu).  Kernels with no registers to spare
+// keep mode 0 or 1.
+template <int SIGN, bool PRE = false, int TW2 = 2, class Bar, class PreWrite = NoHook>
 __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
                                              Bar bar, PreWrite pre_write = PreWrite(),
                                              double2 pre = make_double2(1.0, 0.0)) {
@@ -412,18 +442,31 @@ __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int
     } else {
         apply_pow_twiddles<16, SIGN>(v, T.tb + tid);
     }
+    const int g = fft2l_g(tid), u = fft2l_u(tid), sw = fft2l_swz(g);
+    double2 q1, q2, q4, q8;
+    if constexpr (TW2 == 2) {
+        q1 = tw_sign<SIGN>(T.t16[16 + u]), q2 = tw_sign<SIGN>(T.t16[32 + u]);
+        q4 = tw_sign<SIGN>(T.t16[64 + u]), q8 = tw_sign<SIGN>(T.t16[128 + u]);
+    }
     pre_write();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 256 + (tid ^ fft2l_swz(k1))] = v[k1];
     bar();
-    const int g = fft2l_g(tid), u = fft2l_u(tid), sw = fft2l_swz(g);
     double2* reg = buf + g * 256;
     const double2* rd1 = reg + (u ^ sw);
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = rd1[16 * m];
+    if constexpr (TW2 == 1) {
+        q1 = tw_sign<SIGN>(T.t16[16 + u]), q2 = tw_sign<SIGN>(T.t16[32 + u]);
+        q4 = tw_sign<SIGN>(T.t16[64 + u]), q8 = tw_sign<SIGN>(T.t16[128 + u]);
+    }
     dft<16, SIGN>(v);
+    if constexpr (TW2 == 0) {
 #pragma unroll
-    for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], tw_sign<SIGN>(T.t16[a * 16 + u]));
+        for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], tw_sign<SIGN>(T.t16[a * 16 + u]));
+    } else {
+        apply_pow_twiddles_regs(v, q1, q2, q4, q8);
+    }
     __syncwarp();
     const int U = u ^ sw;
 #pragma unroll

@@ -34,6 +34,14 @@
 #include "plans.hpp"
 #include "tmem.cuh"
 
+// second-level twiddle mode of block_fft_2l (fft_block.cuh) per kernel
+#ifndef NB_P1_TW2
+#define NB_P1_TW2 2
+#endif
+#ifndef NB_P2_TW2
+#define NB_P2_TW2 0
+#endif
+
 namespace nb {
 
 namespace {
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             }
             gsync();  // previous term's last-stage reads of buf are done
             if constexpr (F2L) {
-                block_fft_2l<-1>(v, buf, tid, T, gsync);
+                block_fft_2l<-1, false, 0>(v, buf, tid, T, gsync);
             } else {
                 block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
             }
@@ -334,9 +342,12 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
             tbw[e * 256 + tid] = unit_root(((((long long)tid << p.log_n2) + k2) << e) & (N - 1), N);
-        {
+        if constexpr (NB_P1_TW2 == 0) {
             const long long a = tid >> 4, uu = tid & 15;
             t16c[tid] = unit_root(((uu * (N >> 8) + 16 * k2) * a) & (N - 1), N);
+        } else if (tid < 64) {  // block_fft_2l reads the rows a = 1, 2, 4, 8 only
+            const long long a = 1ll << (tid >> 4), uu = tid & 15;
+            t16c[16 * a + uu] = unit_root(((uu * (N >> 8) + 16 * k2) * a) & (N - 1), N);
         }
         const double two_s0 = (double)(4 * ((((long long)tid) << p.log_n2) + k2)) / (double)N - 2.0;
 #pragma unroll
@@ -396,7 +407,7 @@ __global__ void __launch_bounds__(512, 1)
             // buf must be free (the engine has read the previous term's box) only when the
             // exchange first writes it: wait there, after the first-level DFT, so the TMA
             // drain of the previous column-term overlaps that compute
-            block_fft_2l<-1>(v, buf, tid, T, gsync, [&] {
+            block_fft_2l<-1, false, NB_P1_TW2>(v, buf, tid, T, gsync, [&] {
                 if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 gsync();
             });
@@ -841,7 +852,7 @@ __global__ void __launch_bounds__(G2Shape<L2, SWG>::ALL, 1)
                     for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * G));
                     if (i >= 3) nbar_sync(BAR_EMPTY + b, PAIR);  // gathers of step -3 from b done
                     if constexpr (F2L) {
-                        block_fft_2l<-1>(v, buf, tid, T, gsync);
+                        block_fft_2l<-1, false, 0>(v, buf, tid, T, gsync);
                         // X in place: each thread overwrites only the slots it read last
 #pragma unroll
                         for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
@@ -1055,7 +1066,7 @@ __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int 
     // at the first exchange write, after the first-level DFT, measured slower here:
     // pass 2 2.19 -> 2.44 ms.)
     gsync();
-    block_fft_2l<-1>(v, buf, tid, T, gsync);
+    block_fft_2l<-1, false, NB_P2_TW2>(v, buf, tid, T, gsync);
 #pragma unroll
     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
     gsync();  // X complete
@@ -1262,6 +1273,16 @@ __global__ void __launch_bounds__(512, 1)
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
+#ifdef NB_P2_TRACE
+    long long tr_fft = 0, tr_wait = 0, tr_upd = 0, tr_edge = 0, tr_n = 0, tr_t = clock64(), tr_x;
+    const long long tr_begin = tr_t;
+#define NB_TR(acc)       \
+    tr_x = clock64();    \
+    acc += tr_x - tr_t;  \
+    tr_t = tr_x;
+#else
+#define NB_TR(acc)
+#endif
     int S0 = 0;         // global index of the unit's first step
     bool pre = false;   // this group's first step of the unit is already transformed
     bool have = false;  // v holds this group's next row (loaded ahead)
@@ -1278,9 +1299,11 @@ __global__ void __launch_bounds__(512, 1)
         const bool has_next = row < n1;
         const int last = nt - 1;
         const int lastgrp = (S0 + last) & 1;  // group of the unit's last update
+        NB_TR(tr_edge)
         for (int i = (grp - S0) & 1; i < nt; i += 2) {
             const int rr = last - i;  // term index relative to r0 (r = r1 - 1 - i)
             const int r = p.r1 - 1 - i;
+            NB_TR(tr_edge)
             if (i > 0 || !pre) {
                 if (!have) fs_load_row(v, Y + y_index(rr, N, p.log_n2, urow, 0), tid);
                 fs_fft_regs(v, buf, tid, T, gsync);
@@ -1295,10 +1318,12 @@ __global__ void __launch_bounds__(512, 1)
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt),
                              "r"((unsigned)(2 * 4096 * sizeof(double2))) : "memory");
             }
+            NB_TR(tr_fft)
             if (i > 0) {  // the other group's update of step i-1 is done
                 nbar_sync(BAR_H + (grp ^ 1), 2 * G);
                 tm_fence_after();
             }
+            NB_TR(tr_wait)
             const double rd = (double)r;
 #pragma unroll 1
             for (int k = 0; k < nch; ++k) {
@@ -1340,6 +1365,10 @@ __global__ void __launch_bounds__(512, 1)
             tm_fence_before();
             if (i < last) nbar_arrive(BAR_H + grp, 2 * G);  // hand off step i+1
             else nbar_arrive(BAR_E, 2 * G);                   // unit's last update done
+            NB_TR(tr_upd)
+#ifdef NB_P2_TRACE
+            ++tr_n;
+#endif
         }
         // unit boundary.  The group that did not do the last update transforms the
         // next unit's first row first (its first step), then joins.
@@ -1363,6 +1392,12 @@ __global__ void __launch_bounds__(512, 1)
         }
         S0 += nt;
     }
+#ifdef NB_P2_TRACE
+    NB_TR(tr_edge)
+    if (blockIdx.x == 3 && (tid == 0 || tid == 200))
+        printf("pass2 trace grp %d tid %d: steps %lld, per step: fft %lld wait %lld update %lld; unit edges total %lld of %lld cycles\n",
+               grp, tid, tr_n, tr_fft / tr_n, tr_wait / tr_n, tr_upd / tr_n, tr_edge, tr_t - tr_begin);
+#endif
     tm_fence_before();
     __syncthreads();
     if (threadIdx.x < 32) tm_dealloc(tmem_base, 512u);

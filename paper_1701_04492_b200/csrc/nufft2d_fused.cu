@@ -32,6 +32,14 @@
 #include "plans.hpp"
 #include "tmem.cuh"
 
+// second-level twiddle mode of block_fft_2l (fft_block.cuh) per kernel
+#ifndef NB_2DR_TW2
+#define NB_2DR_TW2 2
+#endif
+#ifndef NB_2DC_TW2
+#define NB_2DC_TW2 2
+#endif
+
 namespace nb {
 
 namespace {
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(LM / 16, 1)
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
                     if constexpr (LM == 4096) {  // two-level FFT, X left in place (fft2l_slot)
-                        block_fft_2l<-1>(v, buf, tid, T, [] { __syncthreads(); });
+                        block_fft_2l<-1, false, NB_2DR_TW2>(v, buf, tid, T, [] { __syncthreads(); });
 #pragma unroll
                         for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
                     } else {
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                     for (int q = 0; q < 16; ++q) v[q] = cscale(rcol[tid + q * G], __ldg(vy + tid + q * G));
                     gsync();  // this group's gathers from buf (its previous step) are done
-                    block_fft_2l<-1>(v, buf, tid, T, gsync);
+                    block_fft_2l<-1, false, NB_2DC_TW2>(v, buf, tid, T, gsync);
 #pragma unroll
                     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
                     gsync();  // X complete

@@ -36,6 +36,14 @@
 #include "plans.hpp"
 #include "tmem.cuh"
 
+// second-level twiddle mode of block_fft_2l (fft_block.cuh) per kernel
+#ifndef NB_PA_TW2
+#define NB_PA_TW2 2
+#endif
+#ifndef NB_PB_TW2
+#define NB_PB_TW2 2
+#endif
+
 namespace nb {
 
 namespace {
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                 if constexpr (F2L) {
                     // the terms must have been read by every bin sum before the exchange
                     // first writes buf: wait there, after the first-level DFT
-                    block_fft_2l<-1>(v, buf, tid, T, gsync, [&] { gsync(); });
+                    block_fft_2l<-1, false, NB_PA_TW2>(v, buf, tid, T, gsync, [&] { gsync(); });
                 } else {
                     gsync();  // terms read before stage 1 reuses buf
                     block_fft_1buf<L2, -1>(v, buf, tid, T, gsync);
@@ -684,9 +692,9 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             if constexpr (TMA) {
                 // the inter-pass twiddle w_N^{k2 (tid + 256 q)} = base * step[q]: step[q] on
                 // the inputs above, the thread constant base with the first-level twiddles
-                block_fft_2l<-1, true>(v, buf, tid, T, gsync, NoHook(), base);
+                block_fft_2l<-1, true, NB_PB_TW2>(v, buf, tid, T, gsync, NoHook(), base);
             } else if constexpr (F2L) {
-                block_fft_2l<-1>(v, buf, tid, T, gsync);
+                block_fft_2l<-1, false, NB_PB_TW2>(v, buf, tid, T, gsync);
             } else {
                 block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
             }
