@@ -229,17 +229,23 @@ void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch,
     // y_r = F1~(v_r .* c) for the first family (the inner type-I transforms of terms
     // [r0, r1)), kept for the single sample-ordered epilogue; the beta family reduces to
     // dot products (D_r) whenever B is non-trivial
-    DevBuf scaled(sizeof(double2) * N, s), Y(sizeof(double2) * N * nt, s), D(sizeof(double2) * K, s);
+    // the inner transforms go to the transpose core kGroup at a time (one stacked pass-A launch
+    // per group when the row FFT is 2048 points, transpose_fused.cu)
+    constexpr size_t kGroup = 4;
+    DevBuf scaled(sizeof(double2) * N * kGroup, s), Y(sizeof(double2) * N * nt, s), D(sizeof(double2) * K, s);
     DevBuf part(p.btrivial ? 16 : sizeof(double2) * kDotBlocks * kDotTerms, s);
     const int deg0 = bessel_series_degree_rel(p.a.gamma_factors, (int)r1 - 1);
     const int deg1 = bessel_series_degree_rel(p.a.gamma_factors, (int)r1);
     for (size_t b = 0; b < batch; ++b) {
         const double2* cb = c + b * N;
-        for (size_t r = r0; r < r1; ++r) {
-            k3_scale<<<blocks(N), 256, 0, s>>>(cb, p.omega.as<double>(), scaled.as<double2>(), (long long)N,
-                                               (int)r, uni);
-            NB_LAUNCH();
-            exec_transpose(p.inner, scaled.as<double2>(), Y.as<double2>() + (r - r0) * N, 1, s);
+        for (size_t g0 = r0; g0 < r1; g0 += kGroup) {
+            const size_t ng = std::min(kGroup, r1 - g0);
+            for (size_t r = g0; r < g0 + ng; ++r) {
+                k3_scale<<<blocks(N), 256, 0, s>>>(cb, p.omega.as<double>(), scaled.as<double2>() + (r - g0) * N,
+                                                   (long long)N, (int)r, uni);
+                NB_LAUNCH();
+            }
+            exec_transpose(p.inner, scaled.as<double2>(), Y.as<double2>() + (g0 - r0) * N, ng, s);
         }
         if (!p.btrivial) {
             for (size_t q0 = r0; q0 < r1; q0 += kDotTerms) {

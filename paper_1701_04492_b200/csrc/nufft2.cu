@@ -41,6 +41,9 @@
 #ifndef NB_P2_TW2
 #define NB_P2_TW2 0
 #endif
+#ifndef NB_P1_LDPIPE
+#define NB_P1_LDPIPE 1
+#endif
 
 namespace nb {
 
@@ -327,6 +330,16 @@ __global__ void __launch_bounds__(512, 1)
     const int warp = tid >> 5, e = tid & 1, u = (tid >> 1) & 15;
     double2* stg = buf + ((warp * 16 + u) * 2 + e);  // + 256 b: staging slot of output b
     const unsigned buf_s = (unsigned)__cvta_generic_to_shared(buf);
+#ifdef NB_P1_TRACE
+    long long t1_set = 0, t1_ld = 0, t1_fft = 0, t1_out = 0, t1_cols = 0, t1_terms = 0, t1_t = clock64(), t1_x;
+    const long long t1_begin = t1_t;
+#define NB_T1(acc)       \
+    t1_x = clock64();    \
+    acc += t1_x - t1_t;  \
+    t1_t = t1_x;
+#else
+#define NB_T1(acc)
+#endif
     for (long long k2 = 2ll * blockIdx.x + grp; k2 < n2; k2 += 2ll * gridDim.x) {
         gsync();  // previous column's readers of step / t16c are done
         // The inter-pass twiddle w_N^{k2 t1} of output t1 = g + 16 a + 256 b of the
@@ -378,14 +391,38 @@ __global__ void __launch_bounds__(512, 1)
         }
         tm_wait_st();
         gsync();  // step visible
+        NB_T1(t1_set)
+#ifdef NB_P1_TRACE
+        ++t1_cols;
+#endif
+        NB_T1(t1_set)
+#ifdef NB_P1_TRACE
+        ++t1_cols;
+#endif
         for (int r = p.r0; r < p.r1; ++r) {
             double2 v[16];
+#if NB_P1_LDPIPE
+            // TMEM chunk j + 1 is in flight while chunk j is scaled
+            unsigned cvb[2][16], svb[2][16];
+            tm_ld16(tc_c, cvb[0]);
+            tm_ld16(tc_s, svb[0]);
+#endif
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
+#if NB_P1_LDPIPE
+                tm_wait_ld();
+                if (j < 3) {
+                    tm_ld16(tc_c + 16 * (j + 1), cvb[(j + 1) & 1]);
+                    tm_ld16(tc_s + 16 * (j + 1), svb[(j + 1) & 1]);
+                }
+                unsigned(&cv)[16] = cvb[j & 1];
+                unsigned(&sv)[16] = svb[j & 1];
+#else
                 unsigned cv[16], sv[16];
                 tm_ld16(tc_c + 16 * j, cv);
                 tm_ld16(tc_s + 16 * j, sv);
                 tm_wait_ld();
+#endif
 #pragma unroll
                 for (int uu = 0; uu < 4; ++uu) {
                     const int q = 4 * j + uu;
@@ -404,6 +441,7 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 if (r > 0) tm_st16(tc_s + 16 * j, sv);
             }
+            NB_T1(t1_ld)
             // buf must be free (the engine has read the previous term's box) only when the
             // exchange first writes it: wait there, after the first-level DFT, so the TMA
             // drain of the previous column-term overlaps that compute
@@ -412,6 +450,7 @@ __global__ void __launch_bounds__(512, 1)
                 gsync();
             });
             gsync();  // exchange reads done: buf becomes the staging box
+            NB_T1(t1_fft)
 #pragma unroll
             for (int b = 0; b < 16; ++b) stg[256 * b] = b == 0 ? v[0] : cmul(v[b], step[b]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -424,9 +463,18 @@ __global__ void __launch_bounds__(512, 1)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
+            NB_T1(t1_out)
+#ifdef NB_P1_TRACE
+            ++t1_terms;
+#endif
         }
         tm_wait_st();
     }
+#ifdef NB_P1_TRACE
+    if (blockIdx.x == 3 && (tid == 0 || tid == 200))
+        printf("pass1 trace grp %d tid %d: columns %lld, per column set-up %lld; per term: tmem-load+scale %lld fft %lld twiddle+stage+tma %lld; total %lld cycles\n",
+               grp, tid, t1_cols, t1_set / t1_cols, t1_ld / t1_terms, t1_fft / t1_terms, t1_out / t1_terms, clock64() - t1_begin);
+#endif
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tm_fence_before();
     __syncthreads();
@@ -1056,8 +1104,13 @@ struct FsShape {
 // load one Y row (stride-2 layout, y_index), transform it and leave X_r in
 // place in the group's buffer (fft2l_slot order)
 __device__ __forceinline__ void fs_load_row(double2 (&v)[16], const double2* row_in, int tid) {
+#ifdef NB_P2_SKIP_LOAD  // timing ablation only (wrong results)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = make_double2(1e-3 * tid + q, (double)(long long)row_in * 1e-18);
+#else
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = __ldcg(row_in + 2 * (tid + q * 256));
+#endif
 }
 template <class Bar>
 __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int tid, const Twiddles<4096>& T,
@@ -1066,7 +1119,9 @@ __device__ __forceinline__ void fs_fft_regs(double2 (&v)[16], double2* buf, int 
     // at the first exchange write, after the first-level DFT, measured slower here:
     // pass 2 2.19 -> 2.44 ms.)
     gsync();
+#ifndef NB_P2_SKIP_FFT  // timing ablation only (wrong results): scripts/gpu_job_trace.sh
     block_fft_2l<-1, false, NB_P2_TW2>(v, buf, tid, T, gsync);
+#endif
 #pragma unroll
     for (int q = 0; q < 16; ++q) buf[fft2l_slot(tid, q)] = v[q];
     gsync();  // X complete
@@ -1275,6 +1330,7 @@ __global__ void __launch_bounds__(512, 1)
     tm_fence_after();
 #ifdef NB_P2_TRACE
     long long tr_fft = 0, tr_wait = 0, tr_upd = 0, tr_edge = 0, tr_n = 0, tr_t = clock64(), tr_x;
+    long long tr_e1 = 0, tr_e2 = 0, tr_e3 = 0, tr_e4 = 0, tr_units = 0;
     const long long tr_begin = tr_t;
 #define NB_TR(acc)       \
     tr_x = clock64();    \
@@ -1325,8 +1381,13 @@ __global__ void __launch_bounds__(512, 1)
             }
             NB_TR(tr_wait)
             const double rd = (double)r;
+#ifdef NB_P2_SKIP_UPD  // timing ablation only (wrong results)
+            const int nch_u = 0;
+#else
+            const int nch_u = nch;
+#endif
 #pragma unroll 1
-            for (int k = 0; k < nch; ++k) {
+            for (int k = 0; k < nch_u; ++k) {
                 unsigned av[4 * CH], gv[4 * CH], hv[2 * CH], t2v[CH];
                 tm_ldn<4 * CH>(tl + W::COL_ACC + 4 * CH * k, av);
                 tm_ldn<2 * CH>(tl + W::COL_H + 2 * CH * k, hv);
@@ -1373,6 +1434,7 @@ __global__ void __launch_bounds__(512, 1)
         // unit boundary.  The group that did not do the last update transforms the
         // next unit's first row first (its first step), then joins.
         pre = false;
+        NB_TR(tr_edge)
         if (grp != lastgrp) {
             if (has_next) {
                 fs_load_row(v, Y + y_index(last, N, p.log_n2, row, 0), tid);
@@ -1382,21 +1444,29 @@ __global__ void __launch_bounds__(512, 1)
             nbar_sync(BAR_E, 2 * G);
             tm_fence_after();
         }
+        NB_TR(tr_e1)
         epi_half(ucb, ucnt);
+        NB_TR(tr_e2)
         if (has_next) {
             init_half(cb, cnt);
             tm_wait_st();
             tm_fence_before();
+            NB_TR(tr_e3)
             nbar_sync(BAR_U, 2 * G);  // next unit's samples set up by both groups
             tm_fence_after();
         }
+        NB_TR(tr_e4)
+#ifdef NB_P2_TRACE
+        ++tr_units;
+#endif
         S0 += nt;
     }
 #ifdef NB_P2_TRACE
     NB_TR(tr_edge)
     if (blockIdx.x == 3 && (tid == 0 || tid == 200))
-        printf("pass2 trace grp %d tid %d: steps %lld, per step: fft %lld wait %lld update %lld; unit edges total %lld of %lld cycles\n",
-               grp, tid, tr_n, tr_fft / tr_n, tr_wait / tr_n, tr_upd / tr_n, tr_edge, tr_t - tr_begin);
+        printf("pass2 trace grp %d tid %d: steps %lld, per step: fft %lld wait %lld update %lld; units %lld, per unit edge: first-fft/wait %lld epilogue %lld init %lld wait %lld other %lld; total %lld cycles\n",
+               grp, tid, tr_n, tr_fft / tr_n, tr_wait / tr_n, tr_upd / tr_n, tr_units, tr_e1 / tr_units, tr_e2 / tr_units,
+               tr_e3 / tr_units, tr_e4 / tr_units, tr_edge / tr_units, tr_t - tr_begin);
 #endif
     tm_fence_before();
     __syncthreads();

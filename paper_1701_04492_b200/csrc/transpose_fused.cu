@@ -60,6 +60,10 @@ struct PassAParams {
     const int* rowoff;
     int deg[kRankCap];
     int conj;  // transform conj(g) (the adjoints: F2~* f = conj(F2~^T conj(f)), transforms.hpp:226-232)
+    // stacked launch (k1_passA_tm without TMA): nb input vectors g + b * gstride share the plan
+    // and write Z + b * zstride; the work units are the (vector, row) pairs
+    int nb;
+    long long gstride, zstride;
 };
 
 struct PassBParams {
@@ -244,7 +248,7 @@ struct PassATmShape {
 // Z row (dims: e pair = 4 doubles, u, warp, b, rr N1 + row), as in k2_pass1_tma.
 template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false, int NW = 2>
 __global__ void __launch_bounds__(NW * (L2 / 16), 1)
-    k1_passA_tm(const double2* __restrict__ g, double2* __restrict__ Z, PassAParams p,
+    k1_passA_tm(const double2* __restrict__ g_all, double2* __restrict__ Z_all, PassAParams p,
                 const __grid_constant__ CUtensorMap zmap) {
     static_assert(!F2L || L2 == 4096, "two-level FFT is 4096-point");
     static_assert(!TMA || F2L, "TMA store needs the two-level output order");
@@ -273,7 +277,11 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
     const long long N = p.n;
     const long long n1 = 1ll << p.log_n1;
     const unsigned mask = (1u << p.log_n2) - 1u;
-    for (long long row = (long long)NW * blockIdx.x + grp; row < n1; row += (long long)NW * gridDim.x) {
+    const long long units = TMA ? n1 : n1 * max(p.nb, 1);  // (vector, row) pairs; TMA rows: one vector
+    for (long long unit = (long long)NW * blockIdx.x + grp; unit < units; unit += (long long)NW * gridDim.x) {
+        const long long row = unit & (n1 - 1), vec = unit >> p.log_n1;
+        const double2* __restrict__ g = g_all + vec * p.gstride;
+        double2* __restrict__ Z = Z_all + vec * p.zstride;
         const int beg = p.rowoff[row], end = p.rowoff[row + 1];
         if (beg == end) {  // empty row: Z_r[row][:] = 0
             for (int r = p.r0; r < p.r1; ++r) {
@@ -846,11 +854,17 @@ int occupancy(const void* fn, int threads, size_t smem) {
     return std::max(1, n);
 }
 
+// nb > 1 (L2 = 2048 only, passA_stackable): nb vectors g + b N -> Z + b (r1 - r0) N in one launch
 template <int L2>
-void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
+void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s,
+                  int nb = 1) {
     const DeviceCtx& ctx = DeviceCtx::get(pl.device);
     constexpr size_t SM = PassAShape<L2>::SMEM;
+    if (nb > 1 && L2 != 2048) throw Error(kInternal, "stacked pass A");
     PassAParams p{};
+    p.nb = nb;
+    p.gstride = (long long)pl.n;
+    p.zstride = (long long)pl.n * (r1 - r0);
     p.conj = conj ? 1 : 0;
     p.n = (long long)pl.n;
     p.log_n1 = pl.bk.log_n1;
@@ -885,7 +899,7 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
         auto f4 = pl.uniform ? k1_passA_tm<L2, true, false, false, 4> : k1_passA_tm<L2, false, false, false, 4>;
         CUtensorMap zmap{};
         set_smem(f4, S4::SMEM);
-        const long long rows = 1ll << pl.bk.log_n1;
+        const long long rows = (1ll << pl.bk.log_n1) * nb;
         const int grid4 = (int)std::min<long long>((rows + 3) / 4, (long long)ctx.sms);
         f4<<<grid4, 4 * (L2 / 16), S4::SMEM, s>>>(g, Z, p, zmap);
         NB_LAUNCH();
@@ -932,7 +946,9 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
     NB_LAUNCH();
 }
 
-void dispatch_passA(int L, const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s) {
+void dispatch_passA(int L, const double2* g, double2* Z, const CorePlan& pl, int r0, int r1, bool conj, cudaStream_t s,
+                    int nb = 1) {
+    if (nb > 1) return launch_passA<2048>(g, Z, pl, r0, r1, conj, s, nb);
     switch (L) {
         case 16: return launch_passA<16>(g, Z, pl, r0, r1, conj, s);
         case 32: return launch_passA<32>(g, Z, pl, r0, r1, conj, s);
@@ -973,10 +989,22 @@ void exec_transpose_fused(const CorePlan& pl, const double2* g, double2* f, size
         NB_CUDA(cudaMemsetAsync(f, 0, sizeof(double2) * N * batch, s));
         return;
     }
-    DevBuf Z(sizeof(double2) * N * (size_t)(r1 - r0), s);
     const int L1 = 1 << pl.bk.log_n1, L2 = 1 << pl.bk.log_n2;
+    // L2 = 2048 (N = 2^22, 2^21): 2048 or 1024 rows over 4 x 148 row workers leave the last wave
+    // of a launch half empty (3.46 rows per worker: 86 %); kStack vectors per pass-A launch
+    // fill it (13.8 rows per worker: 99 %).  Type III runs its K inner transforms this way.
+    constexpr size_t kStack = 4;
+    const size_t stack = (L2 == 2048 && pl.bk.log_n1 > 0 && !ev) ? std::min(batch, kStack) : 1;
+    const size_t zlen = N * (size_t)(r1 - r0);
+    DevBuf Z(sizeof(double2) * zlen * stack, s);
     for (size_t b = 0; b < batch; ++b) {
         if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[0], s));
+        if (stack > 1) {
+            if (b % stack == 0)
+                dispatch_passA(L2, g + b * N, Z.as<double2>(), pl, r0, r1, conj, s, (int)std::min(stack, batch - b));
+            dispatch_passB(L1, Z.as<double2>() + (b % stack) * zlen, f + b * N, pl, r0, r1, conj, s);
+            continue;
+        }
         dispatch_passA(L2, g + b * N, Z.as<double2>(), pl, r0, r1, conj, s);
         if (ev && b == 0) NB_CUDA(cudaEventRecord(ev[1], s));
         if (pl.bk.log_n1 == 0) {
