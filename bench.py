@@ -203,6 +203,27 @@ def fp64_roofline(fp, n: int, K: int, ms: dict):
         return None
 
 
+def smem_roofline(sm, n: int, K: int, ms: dict):
+    """roofline.smem from profiles/smem.json: ncu's shared-memory wavefronts per launch of each
+    kernel (LSU data pipe, one 128-byte wavefront per clock per SM) over the live per-pass
+    times.  The FFT exchanges make this pipe the third co-limit beside FP64 issue and HBM."""
+    try:
+        if not sm or sm.get("n") != n or sm.get("K") != K:
+            return None
+        peak = float(sm["peak_wavefronts_per_s"])
+        per = {}
+        for name, ms_k in ms.items():
+            ent = next((v for k, v in sm["kernels"].items() if k.startswith(name)), None)
+            if ent and ms_k > 0:
+                rate = ent["lsu_shared_wavefronts"] / (ms_k / 1e3)
+                per[name] = {"wavefronts_per_launch": ent["lsu_shared_wavefronts"],
+                             "achieved_wavefronts_per_s": rate, "frac_of_smem_peak": rate / peak}
+        return {"peak_wavefronts_per_s": peak, "peak_source": sm.get("peak_source"),
+                "capture": sm.get("capture"), "per_kernel": per}
+    except Exception:  # evidence, not the measurement
+        return None
+
+
 def algorithmic_bytes(n: int, K: int, batch: int):
     """bytes_II = B*16N (c) + B*16N (f) + 12N (x + index) + B*32*K*N."""
     pass1 = batch * (16 * n + 16 * K * n)            # c read once, K spectra written
@@ -405,6 +426,9 @@ def run_ours(args):
     fp = fp64_roofline(load_profile("fp64.json"), n, K, {"k2_pass1": ms1, "k2_pass2": ms2})
     if fp:
         roofline["fp64"] = fp
+    sm = smem_roofline(load_profile("smem.json"), n, K, {"k2_pass1": ms1, "k2_pass2": ms2})
+    if sm:
+        roofline["smem"] = sm
 
     # ---- e2e (1): the host-pointer C-ABI call with pinned buffers, copies inside.  One
     # step = one exec_host call on eb c vectors (cfg2's batch of 8 sharing x): the call

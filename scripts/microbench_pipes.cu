@@ -57,9 +57,11 @@ __global__ void k_dadd(double* out, double a, long long* cyc) {
 }
 
 // LDS.128 / STS.128 conflict-free (consecutive 16-byte slots per lane)
+// (4096 slots: with 2048 the q and q + 8 accesses aliased and the compiler merged them, which
+// doubled the printed rates — 253 / 224 B/clk instead of the real 128 / 112)
 __global__ void k_lds128(double* out, long long* cyc) {
-    __shared__ double2 buf[2048];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_double2(i, -i);
+    extern __shared__ double2 buf[];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = make_double2(i, -i);
     __syncthreads();
     double2 acc = make_double2(0, 0);
     const int base = threadIdx.x & 255;
@@ -67,7 +69,7 @@ __global__ void k_lds128(double* out, long long* cyc) {
     for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const double2 v = buf[(base + q * 256 + it) & 2047];
+            const double2 v = buf[(base + q * 256 + it) & 4095];
             acc.x += v.x;
             acc.y -= v.y;
         }
@@ -78,14 +80,14 @@ __global__ void k_lds128(double* out, long long* cyc) {
 }
 
 __global__ void k_sts128(double* out, long long* cyc) {
-    __shared__ double2 buf[2048];
+    extern __shared__ double2 buf[];
     const int base = threadIdx.x & 255;
     double2 v = make_double2(threadIdx.x, 1.0);
     const long long t0 = clock64();
     for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            buf[(base + q * 256 + it) & 2047] = v;
+            buf[(base + q * 256 + it) & 4095] = v;
             v.x += 1.0;
         }
     }
@@ -127,6 +129,8 @@ int main() {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    CK(cudaFuncSetAttribute(k_lds128, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    CK(cudaFuncSetAttribute(k_sts128, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     double fp64_ops_per_clk_sm = 0, fp64_ops_per_s = 0, sm_ghz = 0;
     for (int test = 0; test < 5; ++test) {
         const char* name = "";
@@ -136,8 +140,8 @@ int main() {
             switch (test) {
                 case 0: k_dfma<<<blocks, threads>>>(out, 0.999999, 1e-9, cyc); name = "DFMA"; break;
                 case 1: k_dadd<<<blocks, threads>>>(out, 1e-9, cyc); name = "DADD"; break;
-                case 2: k_lds128<<<blocks, threads>>>(out, cyc); name = "LDS.128"; break;
-                case 3: k_sts128<<<blocks, threads>>>(out, cyc); name = "STS.128"; break;
+                case 2: k_lds128<<<blocks, threads, 65536>>>(out, cyc); name = "LDS.128"; break;
+                case 3: k_sts128<<<blocks, threads, 65536>>>(out, cyc); name = "STS.128"; break;
                 case 4: k_shfl<<<blocks, threads>>>(out, cyc); name = "SHFL.32"; break;
             }
             CK(cudaEventRecord(e1));

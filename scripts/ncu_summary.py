@@ -45,7 +45,7 @@ def val(d, k):
 
 
 lines = []
-traffic, fp64 = {}, {}
+traffic, fp64, smem = {}, {}, {}
 for name, ds in per.items():
     lines.append(f"== {name}  ({len(ds)} launches captured; per-launch means)")
     for k in keys:
@@ -54,6 +54,9 @@ for name, ds in per.items():
             lines.append(f"  {k:65s} {v:.6g} {units[ix[k]] if 'bytes' not in k and 'duration' not in k else ''}")
     t = sum(val(d, "dram__bytes_read.sum") + val(d, "dram__bytes_write.sum") for d in ds) / len(ds)
     traffic[name] = t
+    if "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum" in ix:
+        wf = sum(val(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") for d in ds) / len(ds)
+        smem[name] = {"lsu_shared_wavefronts": wf, "per_point_term": wf / (n * K)}
     # FP64 thread instructions from the SASS source page
     base = name.split("<")[0].replace("void ", "").strip()
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{base}"],
@@ -98,6 +101,13 @@ print("\n".join(lines))
 if not write_json:
     sys.exit(0)
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+# shared-memory pipe: one 128-byte wavefront per clock per SM (LDS.128 127.9 B/clk/SM measured,
+# scripts/microbench_fft8.cu); the bench divides by the live kernel time
+json.dump({"n": n, "K": K, "kernels": smem, "peak_wavefronts_per_s": 148 * 1.965e9,
+           "peak_source": "1 shared-memory wavefront (128 B) per clock per SM: LDS.128 127.9 B/clk/SM, STS.128 "
+                          "111.9 B/clk/SM measured (scripts/microbench_fft8.cu) x 148 SMs x 1965 MHz",
+           "capture": os.path.basename(rep)},
+          open(os.path.join(ROOT, "profiles", "smem.json"), "w"), indent=1)
 peak_file = os.path.join(ROOT, "profiles", "r2_microbench_pipes.txt")
 per_clk, clk = 63.37, 1.965e9
 try:

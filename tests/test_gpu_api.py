@@ -213,7 +213,26 @@ def test_batched_exec_equals_singles_all_types(nb):
         assert torch.equal(torch.view_as_real(fs), torch.view_as_real(fb[b]))
 
 
-@pytest.mark.gpu
+def test_stacked_passA_equals_singles(nb):
+    """N = 2^21 (row FFT 2048, 1024 rows): batch > 1 runs pass A of the transpose core as
+    ONE stacked launch per four vectors (transpose_fused.cu, the path type III uses for its
+    inner transforms); a batch of 5 (groups of 4 + 1) must be bit-identical to five single
+    executions, which take the unstacked launches."""
+    import torch
+    n = 1 << 21
+    rng = np.random.default_rng(2121)
+    w = np.clip(np.arange(n) + rng.uniform(-0.45, 0.45, n), 0, n)
+    p1 = nb.plan_nufft1(w, 1e-9)
+    dev = torch.device("cuda", 0)
+    cs = torch.randn(5, n, dtype=torch.complex128, device=dev)
+    fb = torch.empty_like(cs)
+    p1.execute_device(cs.data_ptr(), fb.data_ptr(), 5)
+    for b in range(5):
+        fs = torch.empty_like(cs[b])
+        p1.execute_device(cs[b].data_ptr(), fs.data_ptr(), 1)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.view_as_real(fs), torch.view_as_real(fb[b])), b
+
 @pytest.mark.parametrize("logn", [14, 24])
 def test_type2_host_batch_pipelined_equals_singles(nb, logn):
     """exec_host with batch > 1 streams the vectors through two device slots on three
