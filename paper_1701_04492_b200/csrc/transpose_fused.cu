@@ -43,6 +43,12 @@
 #ifndef NB_PB_TW2
 #define NB_PB_TW2 2
 #endif
+#ifndef NB_PB_PF
+#define NB_PB_PF 0  // next-term register prefetch at L1 = 2048: measured slower (cfg4 22.9 -> 24.1 ms)
+#endif
+#ifndef NB_PA_BINS
+#define NB_PA_BINS 1
+#endif
 
 namespace nb {
 
@@ -425,7 +431,13 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                     }
                 }
                 gsync();  // terms visible
+                // bin sums in ascending j.  Sixteen bins per thread, about one sample per bin:
+                // all bin ranges first, then every bin's first and second term as two batches
+                // of independent (predicated) loads, and a loop only for bins with three or
+                // more samples — sixteen dependent range -> term -> branch chains in sequence
+                // were 22 % of this kernel's stall samples at cfg4 (r2_ncu_type3_s5.txt)
                 double2 v[16];
+#if !NB_PA_BINS
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     const unsigned rb = bo[tid + q * G];
@@ -437,6 +449,30 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                     }
                     v[q] = acc;
                 }
+#else
+                unsigned rbv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) rbv[q] = bo[tid + q * G];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
+                    v[q] = i0 < i1 ? buf[i0] : make_double2(0.0, 0.0);
+                }
+                bool more = false;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
+                    if (i0 + 1 < i1) v[q] = cadd(v[q], buf[i0 + 1]);
+                    more |= i0 + 2 < i1;
+                }
+                if (more) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
+                        for (int i = i0 + 2; i < i1; ++i) v[q] = cadd(v[q], buf[i]);
+                    }
+                }
+#endif
                 if constexpr (F2L) {
                     // the terms must have been read by every bin sum before the exchange
                     // first writes buf: wait there, after the first-level DFT
@@ -675,6 +711,16 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             }
         }
         gsync();  // step visible
+        // L1 = 2048 runs 256 threads per CTA (registers to spare): the next term's column is
+        // loaded into nx while this term transforms, instead of 16 exposed strided loads per
+        // term (long-scoreboard stalls were 30 % of this kernel at cfg4)
+        constexpr bool PF = NB_PB_PF && !TMA && L1 == 2048;
+        double2 nx[PF ? 16 : 1];
+        if constexpr (PF) {
+            const double2* col = Z + k2;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) nx[q] = __ldcg(col + ((long long)(tid + q * G) << p.log_n2));
+        }
         for (int r = p.r0; r < p.r1; ++r) {
             double2 v[16];
             if constexpr (TMA) {
@@ -685,6 +731,14 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 col_phase ^= 1;
 #pragma unroll
                 for (int q = 8; q < 16; ++q) v[q] = cmul(buf[tid + (q - 8) * G], step[q]);
+            } else if constexpr (PF) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = cmul(nx[q], cmul(base, step[q]));
+                if (r + 1 < p.r1) {
+                    const double2* col = Z + (long long)(r + 1 - p.r0) * N + k2;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) nx[q] = __ldcg(col + ((long long)(tid + q * G) << p.log_n2));
+                }
             } else {
                 const double2* col = Z + (long long)(r - p.r0) * N + k2;
 #pragma unroll
