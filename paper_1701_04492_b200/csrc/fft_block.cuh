@@ -387,6 +387,34 @@ __device__ __forceinline__ void apply_pow_twiddles_regs(double2* a, double2 p1, 
     a[15] = cmul(a[15], cmul(p7, p8));
 }
 
+// the same products with at most five factors live at a time (p1, p2, p4, p8 and one of p3, p5,
+// p6, p7), for kernels at the register limit
+__device__ __forceinline__ void apply_pow_twiddles_lowreg(double2* a, double2 p1, double2 p2, double2 p4, double2 p8) {
+    a[8] = cmul(a[8], p8);
+    a[1] = cmul(a[1], p1);
+    a[9] = cmul(a[9], cmul(p1, p8));
+    a[2] = cmul(a[2], p2);
+    a[10] = cmul(a[10], cmul(p2, p8));
+    a[4] = cmul(a[4], p4);
+    a[12] = cmul(a[12], cmul(p4, p8));
+    {
+        const double2 p5 = cmul(p1, p4);
+        a[5] = cmul(a[5], p5);
+        a[13] = cmul(a[13], cmul(p5, p8));
+    }
+    {
+        const double2 p6 = cmul(p2, p4);
+        a[6] = cmul(a[6], p6);
+        a[14] = cmul(a[14], cmul(p6, p8));
+    }
+    const double2 p3 = cmul(p1, p2);
+    a[3] = cmul(a[3], p3);
+    a[11] = cmul(a[11], cmul(p3, p8));
+    const double2 p7 = cmul(p3, p4);
+    a[7] = cmul(a[7], p7);
+    a[15] = cmul(a[15], cmul(p7, p8));
+}
+
 // PreWrite: called once, after the first-level DFT and twiddles and before the
 // first write to buf — the point by which buf must be free (callers whose
 // buf is still being read by the TMA engine wait there, not before the FFT).
@@ -444,7 +472,7 @@ __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int
     }
     const int g = fft2l_g(tid), u = fft2l_u(tid), sw = fft2l_swz(g);
     double2 q1, q2, q4, q8;
-    if constexpr (TW2 == 2) {
+    if constexpr (TW2 == 2 || TW2 == 4) {
         q1 = tw_sign<SIGN>(T.t16[16 + u]), q2 = tw_sign<SIGN>(T.t16[32 + u]);
         q4 = tw_sign<SIGN>(T.t16[64 + u]), q8 = tw_sign<SIGN>(T.t16[128 + u]);
     }
@@ -464,6 +492,13 @@ __device__ __forceinline__ void block_fft_2l(double2 (&v)[16], double2* buf, int
     if constexpr (TW2 == 0) {
 #pragma unroll
         for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], tw_sign<SIGN>(T.t16[a * 16 + u]));
+    } else if constexpr (TW2 == 3) {
+        // the four bases loaded only now, applied in an order that keeps five factors live
+        const double2 b8 = tw_sign<SIGN>(T.t16[128 + u]), b1 = tw_sign<SIGN>(T.t16[16 + u]);
+        const double2 b2 = tw_sign<SIGN>(T.t16[32 + u]), b4 = tw_sign<SIGN>(T.t16[64 + u]);
+        apply_pow_twiddles_lowreg(v, b1, b2, b4, b8);
+    } else if constexpr (TW2 == 4) {
+        apply_pow_twiddles_lowreg(v, q1, q2, q4, q8);
     } else {
         apply_pow_twiddles_regs(v, q1, q2, q4, q8);
     }
