@@ -314,6 +314,12 @@ void finish_core(CorePlan& p, double gamma_for_factors, cudaStream_t s) {
     if (p.fused) build_buckets(p, s);
 }
 
+// flag[0] = 1 when three consecutive sorted keys are equal (a bin with >= 3 samples)
+__global__ void k_crowded_bins(const unsigned* __restrict__ skey, long long n, int* __restrict__ flag) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i + 2 < n && skey[i] == skey[i + 2]) flag[0] = 1;
+}
+
 void build_buckets(CorePlan& p, cudaStream_t s) {
     const size_t n = p.n;
     const int l = ilog2(n);
@@ -350,6 +356,15 @@ void build_buckets(CorePlan& p, cudaStream_t s) {
     p.bk.rowoff_host.resize(n1 + 1);  // row ranges -> sample ranges on the host (multi-GPU chunking)
     NB_CUDA(cudaMemcpyAsync(p.bk.rowoff_host.data(), p.bk.rowoff.as<int>(), 4 * (n1 + 1),
                             cudaMemcpyDeviceToHost, s));
+    {   // bin occupancy class for the transpose core's bin sums (transpose_fused.cu)
+        DevBuf flag(sizeof(int), s);
+        NB_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+        k_crowded_bins<<<blocks(n), 256, 0, s>>>(keys_out.as<unsigned>(), (long long)n, flag.as<int>());
+        NB_LAUNCH();
+        p.bk.crowded.assign(1, 1);
+        NB_CUDA(cudaMemcpyAsync(p.bk.crowded.data(), flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        NB_CUDA(cudaStreamSynchronize(s));  // flag is released below; the plan call synchronizes anyway
+    }
     p.bk.invperm.alloc(4 * n);
     k_invert_perm<<<blocks(n), 256, 0, s>>>(p.bk.perm.as<int>(), (long long)n, p.bk.invperm.as<int>());
     NB_LAUNCH();

@@ -45,6 +45,7 @@ struct Buckets {
     DevArray sort_perm;          // generic transpose core: samples sorted by t (int32)
     DevArray bin_off;            // generic transpose core: N+1 offsets (int32)
     std::vector<int> rowoff_host;  // host copy of rowoff (row chunk -> sample range)
+    std::vector<int> crowded;      // [0] != 0: some bin holds three or more samples (pass A's bin-sum depth)
 };
 
 // Type-I/II core plan: a sample axis, a rank, and the factor parameters.

@@ -50,6 +50,7 @@
 #define NB_PA_BINS 1
 #endif
 
+
 namespace nb {
 
 namespace {
@@ -252,7 +253,10 @@ struct PassATmShape {
 // engine — the z values are staged conflict-free in the exchange buffer in the
 // order (b, warp, u, e) and one 5-D cp.async.bulk.tensor store writes the 64 KiB
 // Z row (dims: e pair = 4 doubles, u, warp, b, rr N1 + row), as in k2_pass1_tma.
-template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false, int NW = 2>
+// BD: terms per bin summed as batches of independent loads before the residual loop — 2 when
+// no bin of the plan holds more than two samples (jittered grids: cfg3 4.01 vs 4.09 ms), 4
+// otherwise (iid samples: the adjoint 5.47 -> 5.24 ms, cfg4 22.9 -> 22.1 ms)
+template <int L2, bool UNIFORM, bool F2L = false, bool TMA = false, int NW = 2, int BD = 2>
 __global__ void __launch_bounds__(NW * (L2 / 16), 1)
     k1_passA_tm(const double2* __restrict__ g_all, double2* __restrict__ Z_all, PassAParams p,
                 const __grid_constant__ CUtensorMap zmap) {
@@ -460,16 +464,19 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                 }
                 bool more = false;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
-                    if (i0 + 1 < i1) v[q] = cadd(v[q], buf[i0 + 1]);
-                    more |= i0 + 2 < i1;
+                for (int d = 1; d < BD; ++d) {  // the d-th term of every bin, one batch per d
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
+                        if (i0 + d < i1) v[q] = cadd(v[q], buf[i0 + d]);
+                        if (d == BD - 1) more |= i0 + BD < i1;
+                    }
                 }
                 if (more) {
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
-                        for (int i = i0 + 2; i < i1; ++i) v[q] = cadd(v[q], buf[i]);
+                        for (int i = i0 + BD; i < i1; ++i) v[q] = cadd(v[q], buf[i]);
                     }
                 }
 #endif
@@ -934,10 +941,15 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
         constexpr size_t SMT = PassATmShape<L2>::SMEM;
         // two-level row FFT; Z rows stored by TMA (LSU stores when the tensor map
         // cannot describe Z)
+        const bool crowded = pl.bk.crowded.empty() || pl.bk.crowded[0] != 0;
         auto fnt = pl.uniform ? k1_passA_tm<L2, true, true> : k1_passA_tm<L2, false, true>;
         CUtensorMap zmap{};
-        if (make_z_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0))
+        if (make_z_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0)) {
             fnt = pl.uniform ? k1_passA_tm<L2, true, true, true> : k1_passA_tm<L2, false, true, true>;
+            if (crowded && !pl.uniform) fnt = k1_passA_tm<L2, false, true, true, 2, 4>;
+        } else if (crowded && !pl.uniform) {
+            fnt = k1_passA_tm<L2, false, true, false, 2, 4>;
+        }
         set_smem(fnt, SMT);
         const long long rows = 1ll << pl.bk.log_n1;
         const int gridt = (int)std::min<long long>((rows + 1) / 2, (long long)ctx.sms);
@@ -950,7 +962,9 @@ void launch_passA(const double2* g, double2* Z, const CorePlan& pl, int r0, int 
         // the cfg4 inner type-I transforms 30.3 -> 27.1 ms per type-III exec (a jittered
         // type I at 2^22: 1.44 -> 1.47 ms); two workers measured 1.63 ms
         using S4 = PassATmShape<L2, 4>;
+        const bool crowded = pl.bk.crowded.empty() || pl.bk.crowded[0] != 0;
         auto f4 = pl.uniform ? k1_passA_tm<L2, true, false, false, 4> : k1_passA_tm<L2, false, false, false, 4>;
+        if (crowded && !pl.uniform) f4 = k1_passA_tm<L2, false, false, false, 4, 4>;
         CUtensorMap zmap{};
         set_smem(f4, S4::SMEM);
         const long long rows = (1ll << pl.bk.log_n1) * nb;
