@@ -44,6 +44,12 @@
 #ifndef NB_P1_LDPIPE
 #define NB_P1_LDPIPE 1
 #endif
+// staging the pass-1 box inside each warp's own exchange regions (a __syncwarp instead of a group
+// barrier before the staging writes; box order (e pair, u, b, warp)): measured SLOWER, pass 1
+// 1.56 -> 1.97 ms — the TMA engine drains that box order more slowly than (e pair, u, warp, b)
+#ifndef NB_P1_STAGE_WARP
+#define NB_P1_STAGE_WARP 0
+#endif
 
 namespace nb {
 
@@ -328,7 +334,16 @@ __global__ void __launch_bounds__(512, 1)
     const long long n2 = 1ll << p.log_n2;
     const long long N = p.n;
     const int warp = tid >> 5, e = tid & 1, u = (tid >> 1) & 15;
+#if NB_P1_STAGE_WARP
+    // staging inside the warp's own two exchange regions (slots [512 warp, 512 warp + 512): the
+    // only ones its last exchange read), order (warp, b, u, e): a __syncwarp, not a group
+    // barrier, separates the exchange reads from the staging writes
+    double2* stg = buf + (warp * 512 + u * 2 + e);    // + 32 b: staging slot of output b
+    constexpr int kStgStride = 32;
+#else
     double2* stg = buf + ((warp * 16 + u) * 2 + e);  // + 256 b: staging slot of output b
+    constexpr int kStgStride = 256;
+#endif
     const unsigned buf_s = (unsigned)__cvta_generic_to_shared(buf);
 #ifdef NB_P1_TRACE
     long long t1_set = 0, t1_ld = 0, t1_fft = 0, t1_out = 0, t1_cols = 0, t1_terms = 0, t1_t = clock64(), t1_x;
@@ -449,10 +464,14 @@ __global__ void __launch_bounds__(512, 1)
                 if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 gsync();
             });
+#if NB_P1_STAGE_WARP
+            __syncwarp();  // the warp's exchange reads are done: its regions become its part of the box
+#else
             gsync();  // exchange reads done: buf becomes the staging box
+#endif
             NB_T1(t1_fft)
 #pragma unroll
-            for (int b = 0; b < 16; ++b) stg[256 * b] = b == 0 ? v[0] : cmul(v[b], step[b]);
+            for (int b = 0; b < 16; ++b) stg[kStgStride * b] = b == 0 ? v[0] : cmul(v[b], step[b]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             gsync();  // box complete
 #ifdef NB_P1_SKIP_TMA  // timing ablation only (no output)
@@ -463,7 +482,11 @@ __global__ void __launch_bounds__(512, 1)
                 asm volatile(
                     "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
                         &ymap),
+#if NB_P1_STAGE_WARP
+                    "r"(0), "r"(0), "r"(16 * (r - p.r0)), "r"(0), "r"((int)k2), "r"(buf_s)
+#else
                     "r"(0), "r"(0), "r"(0), "r"(16 * (r - p.r0)), "r"((int)k2), "r"(buf_s)
+#endif
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
@@ -498,9 +521,16 @@ bool make_y_tensor_map(CUtensorMap* map, double2* Y, int log_n2, int nterms) {
     if (!encode) return false;
     const cuuint64_t n2 = 1ull << log_n2;
     const cuuint64_t row = n2 * 32ull;  // bytes per (t1 >> 1)
+#if NB_P1_STAGE_WARP
+    // box order (e pair, u, b, warp): t1 = e + 2 warp + 16 u + 256 b
+    cuuint64_t dims[5] = {4, 16, 16ull * (cuuint64_t)nterms, 8, n2};
+    cuuint64_t strides[4] = {8 * row, 128 * row, row, 32};
+    cuuint32_t box[5] = {4, 16, 16, 8, 1};
+#else
     cuuint64_t dims[5] = {4, 16, 8, 16ull * (cuuint64_t)nterms, n2};
     cuuint64_t strides[4] = {8 * row, row, 128 * row, 32};
     cuuint32_t box[5] = {4, 16, 8, 16, 1};
+#endif
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     const CUresult rc = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Y, dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
