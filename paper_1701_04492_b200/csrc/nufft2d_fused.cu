@@ -34,10 +34,10 @@
 
 // second-level twiddle mode of block_fft_2l (fft_block.cuh) per kernel
 #ifndef NB_2DR_TW2
-#define NB_2DR_TW2 2
+#define NB_2DR_TW2 4
 #endif
 #ifndef NB_2DC_TW2
-#define NB_2DC_TW2 2
+#define NB_2DC_TW2 4
 #endif
 
 namespace nb {
