@@ -179,12 +179,21 @@ def main():
         sd = torch.empty_like(fd)
         nb.inufft2_device(p, fd.data_ptr(), 1e-10, sd.data_ptr(), op, sh)  # warm-up solve
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        r = nb.inufft2_device(p, fd.data_ptr(), 1e-10, sd.data_ptr(), op, sh)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        # median of five solves (a solve is 30 CG iterations with two host round trips each:
+        # single samples ranged 36-144 ms across runs of this sweep, 35-36 ms when repeated,
+        # scripts/probe_inv2_variance.py)
+        from bench import ClockSampler
+        solves = []
+        with ClockSampler(torch.cuda.current_device()) as cs:
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                r = nb.inufft2_device(p, fd.data_ptr(), 1e-10, sd.data_ptr(), op, sh)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                solves.append(e0.elapsed_time(e1))
+        _CLOCKS["last"] = cs.summary()
+        ms = float(np.median(solves))
         err = float(torch.linalg.norm(sd.cpu() - torch.from_numpy(c)) / np.linalg.norm(c))
         t0 = time.perf_counter()
         nb.inufft2(p, f, 1e-10, op)
@@ -192,7 +201,8 @@ def main():
         emit("inv2", "inverse NUFFT-II N=2^22 jittered (gamma 1/4), tol 1e-10 (device pointers)", n, ms, None,
              p.rank(), ps, {"cg_iterations": r["iterations"], "converged": r["converged"],
                             "rel_error_vs_truth": err, "ms_per_cg_iteration": ms / max(1, r["iterations"]),
-                            "host_api_ms": host_ms, "toeplitz_build_seconds": ps})
+                            "host_api_ms": host_ms, "toeplitz_build_seconds": ps,
+                            "solve_ms_all": [round(t, 2) for t in solves]})
         del p, op, fd, sd
         torch.cuda.empty_cache()
 
