@@ -46,6 +46,9 @@
 #ifndef NB_PB_PF
 #define NB_PB_PF 0  // next-term register prefetch at L1 = 2048: measured slower (cfg4 22.9 -> 24.1 ms)
 #endif
+#ifndef NB_PB_TMA2048
+#define NB_PB_TMA2048 1
+#endif
 #ifndef NB_PA_BINS
 #define NB_PA_BINS 1
 #endif
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     k1_passB_tm(const double2* __restrict__ Z, double2* __restrict__ f, PassBParams p,
                 const __grid_constant__ CUtensorMap zmap) {
     static_assert(!F2L || L1 == 4096, "two-level FFT is 4096-point");
-    static_assert(!TMA || F2L, "TMA load path is for the two-level kernel");
+    static_assert(!TMA || F2L || L1 == 2048, "TMA load path: the two-level kernel, or whole 2048-point columns");
     constexpr int G = L1 / 16;
     extern __shared__ __align__(1024) double2 smem[];
     __shared__ unsigned tmem_base;
@@ -651,6 +654,9 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     // the column of a term arrives in two 32 KiB halves: t1 < 2048 into a dedicated
     // buffer `pre` (issued a whole term ahead), t1 >= 2048 into the exchange buffer
     // (issued once the previous FFT has released it)
+    // TMA without F2L (L1 = 2048): the whole 32 KiB column lands in `pre`, a term ahead; the
+    // 16-byte loads at a 32 KiB stride it replaces cost the LSU one tag lookup per element
+    // (2048 cycles per column-term and worker, 40 % of this kernel at cfg4)
     double2* pre = smem + 2 * padded_len(L1) + 32 + FftShapeX<L1>::TW_LEN + grp * 2048;
     const unsigned bar_s0 = (unsigned)__cvta_generic_to_shared(&colbar[2 * grp]);
     const unsigned bar_s1 = (unsigned)__cvta_generic_to_shared(&colbar[2 * grp + 1]);
@@ -714,7 +720,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             gsync();  // the previous column's last exchange reads of buf / pre are done
             if (tid == 0) {
                 col_load(0, 0, k2);
-                col_load(1, 0, k2);
+                if constexpr (F2L) col_load(1, 0, k2);
             }
         }
         gsync();  // step visible
@@ -730,7 +736,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
         }
         for (int r = p.r0; r < p.r1; ++r) {
             double2 v[16];
-            if constexpr (TMA) {
+            if constexpr (TMA && F2L) {
                 col_wait(bar_s0, col_phase);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) v[q] = q == 0 ? pre[tid] : cmul(pre[tid + q * G], step[q]);
@@ -738,6 +744,11 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 col_phase ^= 1;
 #pragma unroll
                 for (int q = 8; q < 16; ++q) v[q] = cmul(buf[tid + (q - 8) * G], step[q]);
+            } else if constexpr (TMA) {
+                col_wait(bar_s0, col_phase);
+                col_phase ^= 1;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = cmul(pre[tid + q * G], cmul(base, step[q]));
             } else if constexpr (PF) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) v[q] = cmul(nx[q], cmul(base, step[q]));
@@ -758,7 +769,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             if constexpr (TMA) {
                 if (tid == 0 && r + 1 < p.r1) col_load(0, r + 1 - p.r0, k2);  // pre is free: a whole term ahead
             }
-            if constexpr (TMA) {
+            if constexpr (TMA && F2L) {
                 // the inter-pass twiddle w_N^{k2 (tid + 256 q)} = base * step[q]: step[q] on
                 // the inputs above, the thread constant base with the first-level twiddles
                 block_fft_2l<-1, true, NB_PB_TW2>(v, buf, tid, T, gsync, NoHook(), base);
@@ -767,7 +778,7 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
             } else {
                 block_fft_1buf<L1, -1>(v, buf, tid, T, gsync);
             }
-            if constexpr (TMA) {
+            if constexpr (TMA && F2L) {
                 if (r + 1 < p.r1) {
                     gsync();  // exchange reads done: the next term's second half may land in buf
                     if (tid == 0) col_load(1, r + 1 - p.r0, k2);
@@ -863,7 +874,7 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
 
 // Z columns (rr*N + t1*4096 + k2, N1 = 2^log_n1 rows) as the 5-D tensor k1_passB_tm<.., TMA>
 // loads from: (re/im, t1 & 255, t1 >> 8, rr, k2), box = half a column of one term
-bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int nterms) {
+bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int log_n2, int nterms) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -872,11 +883,13 @@ bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int nt
             return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
         return (PFN_cuTensorMapEncodeTiled_v12000)fn;
     }();
-    if (!encode || log_n1 != 12) return false;
-    const cuuint64_t row = 4096ull * 16ull;  // bytes per t1 (N2 = 4096)
-    cuuint64_t dims[5] = {2, 256, 16, (cuuint64_t)nterms, 4096};
-    cuuint64_t strides[4] = {row, 256 * row, 4096 * row, 16};
-    cuuint32_t box[5] = {2, 256, 8, 1, 1};  // half a column (t1 < 2048 or >= 2048)
+    if (!encode || (log_n1 != 12 && log_n1 != 11)) return false;
+    const cuuint64_t n1 = 1ull << log_n1, n2 = 1ull << log_n2;
+    const cuuint64_t row = n2 * 16ull;  // bytes per t1
+    // a box is 2048 pieces of 16 B (32 KiB): half a column at N1 = 4096, a whole one at 2048
+    cuuint64_t dims[5] = {2, 256, n1 / 256, (cuuint64_t)nterms, n2};
+    cuuint64_t strides[4] = {row, 256 * row, n1 * row, 16};
+    cuuint32_t box[5] = {2, 256, 8, 1, 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Z, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -989,10 +1002,17 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         PassBParams p{(long long)pl.n, pl.bk.log_n1, pl.bk.log_n2, r0, r1, conj ? 1 : 0};
         auto fn = pl.uniform ? k1_passB_tm<L1, true> : k1_passB_tm<L1, false>;
         CUtensorMap zmap{};
+        if constexpr (L1 == 2048) {
+            // Z columns (32 KiB) loaded by TMA a term ahead
+            if (NB_PB_TMA2048 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, pl.bk.log_n2, r1 - r0)) {
+                fn = pl.uniform ? k1_passB_tm<L1, true, false, true> : k1_passB_tm<L1, false, false, true>;
+                SMT += sizeof(double2) * 2 * 2048;  // the two `pre` column buffers
+            }
+        }
         if constexpr (L1 == 4096) {
             // two-level column FFT; Z columns loaded by TMA when N2 = 4096
             fn = pl.uniform ? k1_passB_tm<L1, true, true> : k1_passB_tm<L1, false, true>;
-            if (pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, r1 - r0)) {
+            if (pl.bk.log_n2 == 12 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, pl.bk.log_n2, r1 - r0)) {
                 fn = pl.uniform ? k1_passB_tm<L1, true, true, true> : k1_passB_tm<L1, false, true, true>;
                 SMT += sizeof(double2) * 2 * 2048;  // the two `pre` half-column buffers
             }
