@@ -49,6 +49,9 @@
 #ifndef NB_PB_TMA2048
 #define NB_PB_TMA2048 1
 #endif
+#ifndef NB_PB_QL
+#define NB_PB_QL 0  // inputs per thread loaded through the LSU instead of the TMA box (even, 0..8): cfg4 19.07 / 19.40 / 19.98 / 20.49 ms at 0 / 2 / 4 / 6
+#endif
 #ifndef NB_PA_BINS
 #define NB_PA_BINS 1
 #endif
@@ -663,9 +666,14 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
     const unsigned buf_s = (unsigned)__cvta_generic_to_shared(smem + grp * padded_len(L1));
     const unsigned pre_s = (unsigned)__cvta_generic_to_shared(pre);
     int col_phase = 0;
+    // TMA without F2L: the engine moves 0.61 pieces per clock per SM (scripts/microbench_tma_load.cu),
+    // which made a whole 2048-piece column per term the kernel's bound; the last QL of the
+    // thread's 16 inputs (t1 >= 2048 - 128 QL) come through the LSU instead, a term ahead
+    constexpr int QL = (TMA && !F2L) ? NB_PB_QL : 0;
+    constexpr unsigned kBoxBytes = (TMA && !F2L) ? (16 - QL) * 128 * 16 : 32768;
     auto col_load = [&](int half, int rr, long long kk2) {  // thread 0 of the worker
         const unsigned bs = half ? bar_s1 : bar_s0;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bs), "r"(32768) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bs), "r"(kBoxBytes) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
             "%6}], [%7];" ::"r"(half ? buf_s : pre_s),
@@ -734,6 +742,12 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
 #pragma unroll
             for (int q = 0; q < 16; ++q) nx[q] = __ldcg(col + ((long long)(tid + q * G) << p.log_n2));
         }
+        double2 nl[QL > 0 ? QL : 1];
+        if constexpr (QL > 0) {
+            const double2* col = Z + k2;
+#pragma unroll
+            for (int q = 16 - QL; q < 16; ++q) nl[q - (16 - QL)] = __ldcg(col + ((long long)(tid + q * G) << p.log_n2));
+        }
         for (int r = p.r0; r < p.r1; ++r) {
             double2 v[16];
             if constexpr (TMA && F2L) {
@@ -748,7 +762,17 @@ __global__ void __launch_bounds__(2 * (L1 / 16), 1)
                 col_wait(bar_s0, col_phase);
                 col_phase ^= 1;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = cmul(pre[tid + q * G], cmul(base, step[q]));
+                for (int q = 0; q < 16 - QL; ++q) v[q] = cmul(pre[tid + q * G], cmul(base, step[q]));
+                if constexpr (QL > 0) {
+#pragma unroll
+                    for (int q = 16 - QL; q < 16; ++q) v[q] = cmul(nl[q - (16 - QL)], cmul(base, step[q]));
+                    if (r + 1 < p.r1) {
+                        const double2* col = Z + (long long)(r + 1 - p.r0) * N + k2;
+#pragma unroll
+                        for (int q = 16 - QL; q < 16; ++q)
+                            nl[q - (16 - QL)] = __ldcg(col + ((long long)(tid + q * G) << p.log_n2));
+                    }
+                }
             } else if constexpr (PF) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) v[q] = cmul(nx[q], cmul(base, step[q]));
@@ -874,7 +898,7 @@ __global__ void k1_combine(const double2* __restrict__ Z, double2* __restrict__ 
 
 // Z columns (rr*N + t1*4096 + k2, N1 = 2^log_n1 rows) as the 5-D tensor k1_passB_tm<.., TMA>
 // loads from: (re/im, t1 & 255, t1 >> 8, rr, k2), box = half a column of one term
-bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int log_n2, int nterms) {
+bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int log_n2, int nterms, int box_hi = 8) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -889,7 +913,7 @@ bool make_zcol_tensor_map(CUtensorMap* map, const double2* Z, int log_n1, int lo
     // a box is 2048 pieces of 16 B (32 KiB): half a column at N1 = 4096, a whole one at 2048
     cuuint64_t dims[5] = {2, 256, n1 / 256, (cuuint64_t)nterms, n2};
     cuuint64_t strides[4] = {row, 256 * row, n1 * row, 16};
-    cuuint32_t box[5] = {2, 256, 8, 1, 1};
+    cuuint32_t box[5] = {2, 256, (cuuint32_t)box_hi, 1, 1};  // box_hi * 256 pieces
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)Z, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -1004,7 +1028,7 @@ void launch_passB(const double2* Z, double2* f, const CorePlan& pl, int r0, int 
         CUtensorMap zmap{};
         if constexpr (L1 == 2048) {
             // Z columns (32 KiB) loaded by TMA a term ahead
-            if (NB_PB_TMA2048 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, pl.bk.log_n2, r1 - r0)) {
+            if (NB_PB_TMA2048 && make_zcol_tensor_map(&zmap, Z, pl.bk.log_n1, pl.bk.log_n2, r1 - r0, (16 - NB_PB_QL) / 2)) {
                 fn = pl.uniform ? k1_passB_tm<L1, true, false, true> : k1_passB_tm<L1, false, false, true>;
                 SMT += sizeof(double2) * 2 * 2048;  // the two `pre` column buffers
             }
