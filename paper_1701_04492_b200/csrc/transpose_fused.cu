@@ -318,7 +318,29 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                 if (i == 0 || (p.skey[cb + i - 1] & mask) != t2) bo16[2 * t2] = (unsigned short)i;
                 if (i == cnt - 1 || (p.skey[cb + i + 1] & mask) != t2) bo16[2 * t2 + 1] = (unsigned short)(i + 1);
             }
-            // owned samples i = tid + u G: Q = h^r0 G_j (G_j = 2 exp(2ih) g_j), h
+            // owned samples i = tid + u G: Q = h^r0 G_j (G_j = 2 exp(2ih) g_j), h.
+            // Every index, then every gathered value and delta, is loaded before any of them
+            // is used: the TMEM stores below are ordered asm statements, and with the loads
+            // inside the chunk loop each chunk paid its own perm -> g DRAM round trips in turn
+            // (long-scoreboard stalls were 15-17 % of this kernel)
+            int pidx[QA];
+#pragma unroll
+            for (int uu = 0; uu < QA; ++uu) {
+                const int i = tid + uu * G;
+                pidx[uu] = i < cnt ? p.perm[cb + i] : -1;
+            }
+            double2 Gin[QA];
+            double din[QA];
+#pragma unroll
+            for (int uu = 0; uu < QA; ++uu) {
+                const int i = tid + uu * G;
+                Gin[uu] = make_double2(0.0, 0.0);
+                din[uu] = 0.0;
+                if (pidx[uu] >= 0) {
+                    Gin[uu] = __ldg(g + pidx[uu]);
+                    if constexpr (!UNIFORM) din[uu] = p.ds[cb + i];
+                }
+            }
 #pragma unroll
             for (int k = 0; k < (QA + 3) / 4; ++k) {
                 unsigned qv[16], hv[8];
@@ -329,10 +351,10 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                     double2 Gj = make_double2(0.0, 0.0);
                     double h = 0.0;
                     if (uu < QA && i < cnt) {
-                        Gj = __ldg(g + p.perm[cb + i]);
+                        Gj = Gin[uu < QA ? uu : 0];
                         if (p.conj) Gj.y = -Gj.y;
                         if constexpr (!UNIFORM) {
-                            h = half_phase(p.ds[cb + i]);
+                            h = half_phase(din[uu < QA ? uu : 0]);
                             double sn, cs;
                             sincos(2.0 * h, &sn, &cs);
                             Gj = cmul(make_double2(2.0 * cs, 2.0 * sn), Gj);
