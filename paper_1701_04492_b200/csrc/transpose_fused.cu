@@ -504,6 +504,8 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const int i0 = rbv[q] & 0xffffu, i1 = rbv[q] >> 16;
+#pragma unroll 1  // rare: keep it small (unrolled, these 16 loops were a quarter of the kernel's code
+                  // and the kernel stalled 19 % of the time on instruction fetch at N = 2^22)
                         for (int i = i0 + BD; i < i1; ++i) v[q] = cadd(v[q], buf[i]);
                     }
                 }
