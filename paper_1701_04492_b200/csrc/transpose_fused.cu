@@ -354,10 +354,13 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                         Gj = Gin[uu < QA ? uu : 0];
                         if (p.conj) Gj.y = -Gj.y;
                         if constexpr (!UNIFORM) {
-                            h = half_phase(din[uu < QA ? uu : 0]);
-                            double sn, cs;
-                            sincos(2.0 * h, &sn, &cs);
+                            const double dj = din[uu < QA ? uu : 0];
+                            h = half_phase(dj);
+                            double sn, cs;  // exp(2ih) = exp(-i pi delta), argument exact (and
+                                            // sincospi inlines to far less code than sincos)
+                            sincospi(-dj, &sn, &cs);
                             Gj = cmul(make_double2(2.0 * cs, 2.0 * sn), Gj);
+#pragma unroll 1  // a partial term range (multi-GPU) only
                             for (int r = 0; r < p.r0; ++r) Gj = cscale(Gj, h);
                         }
                     }
