@@ -309,6 +309,14 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
         }
         for (int cb = beg, chunk = 0; cb < end; cb += CAP, ++chunk) {
             const int cnt = min(CAP, end - cb);
+            // (the gather indices are requested before the bin table is built: their DRAM round
+            // trip overlaps the key loads below instead of following them)
+            int pidx[QA];
+#pragma unroll
+            for (int uu = 0; uu < QA; ++uu) {
+                const int i = tid + uu * G;
+                pidx[uu] = i < cnt ? p.perm[cb + i] : -1;
+            }
             if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             gsync();  // previous chunk's readers of bo / buf are done
             for (int i = tid; i < L2; i += G) bo[i] = 0u;
@@ -323,12 +331,6 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
             // is used: the TMEM stores below are ordered asm statements, and with the loads
             // inside the chunk loop each chunk paid its own perm -> g DRAM round trips in turn
             // (long-scoreboard stalls were 15-17 % of this kernel)
-            int pidx[QA];
-#pragma unroll
-            for (int uu = 0; uu < QA; ++uu) {
-                const int i = tid + uu * G;
-                pidx[uu] = i < cnt ? p.perm[cb + i] : -1;
-            }
             double2 Gin[QA];
             double din[QA];
 #pragma unroll
