@@ -411,8 +411,9 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
             }
             tm_wait_st();
             for (int r = p.r0; r < p.r1; ++r) {
-                if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                gsync();  // previous term's last-stage reads of buf (and the TMA's) are done
+                // (the wait for the previous term's last-stage reads of buf — and for the TMA
+                // engine to have read its box — sits at the first write of buf below, after the
+                // first eight samples' series: that work overlaps the drain)
                 // term phase: buf[i] = g_r(h_i^2) Q_i, then Q_i <- h_i Q_i.  Two TMEM chunks
                 // (8 samples) share one Horner loop (8 independent FMA chains per coefficient)
                 const double* a = kBes + r * kSeriesTerms;
@@ -458,6 +459,10 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
 #pragma unroll
                             for (int u = 0; u < 8; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
                         }
+                    }
+                    if (k0 == 0) {
+                        if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        gsync();  // previous term's last-stage reads of buf (and the TMA's) are done
                     }
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
