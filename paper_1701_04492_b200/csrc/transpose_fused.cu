@@ -55,6 +55,9 @@
 #ifndef NB_PA_BINS
 #define NB_PA_BINS 1
 #endif
+#ifndef NB_PA_SPLIT_TERM
+#define NB_PA_SPLIT_TERM 1
+#endif
 
 
 namespace nb {
@@ -419,6 +422,90 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                 const double* a = kBes + r * kSeriesTerms;
                 const int deg = p.deg[r];
                 constexpr int NCHK = (QA + 3) / 4;
+#if NB_PA_SPLIT_TERM
+                // T1: the series g_r(h^2) of every owned sample (TMEM and registers only) ...
+                double grv[4 * NCHK];
+#pragma unroll
+                for (int k0 = 0; k0 < NCHK; k0 += 2) {
+                    double w[8], gr[8];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int k = k0 + c;
+                        unsigned hv[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) hv[e] = 0u;
+                        if (k < NCHK) {
+                            if (4 * k + 4 <= QA) {
+                                tm_ld8(tcol + S::COL_H + 8 * k, hv);
+                            } else {
+                                asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                                             : "=r"(hv[0]), "=r"(hv[1])
+                                             : "r"(tcol + S::COL_H + 8 * k)
+                                             : "memory");
+                            }
+                        }
+                        tm_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const double hh = mk64(hv[2 * u], hv[2 * u + 1]);
+                            w[4 * c + u] = hh * hh;
+                        }
+                    }
+                    if constexpr (UNIFORM) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) gr[u] = 1.0;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) gr[u] = a[deg];
+#pragma unroll 1
+                        for (int m = deg - 1; m >= 0; --m) {
+                            const double am = a[m];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) gr[u] = __fma_rn(gr[u], w[u], am);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (4 * k0 + u < 4 * NCHK) grv[4 * k0 + u] = gr[u];
+                }
+                // ... then the wait for buf (previous term's last-stage reads, the TMA drain) ...
+                if (TMA && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                gsync();
+                // ... T2: buf[i] = g_r Q_i, Q_i <- h_i Q_i
+#pragma unroll
+                for (int k = 0; k < NCHK; ++k) {
+                    const bool full = 4 * k + 4 <= QA;
+                    unsigned qv[16], hv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) hv[e] = 0u;
+                    if (full) {
+                        tm_ld16(tcol + S::COL_Q + 16 * k, qv);
+                        if constexpr (!UNIFORM) tm_ld8(tcol + S::COL_H + 8 * k, hv);
+                    } else {
+                        tm_ld4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                        if constexpr (!UNIFORM) tm_ld2(tcol + S::COL_H + 8 * k, hv[0], hv[1]);
+#pragma unroll
+                        for (int e = 4; e < 16; ++e) qv[e] = 0u;
+                    }
+                    tm_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int uu = 4 * k + u;
+                        if (uu >= QA) break;
+                        const double2 Qv = make_double2(mk64(qv[4 * u], qv[4 * u + 1]), mk64(qv[4 * u + 2], qv[4 * u + 3]));
+                        buf[tid + uu * G] = cscale(Qv, grv[uu]);
+                        const double2 Qn = UNIFORM ? Qv : cscale(Qv, mk64(hv[2 * u], hv[2 * u + 1]));
+                        qv[4 * u] = lo32(Qn.x);
+                        qv[4 * u + 1] = hi32(Qn.x);
+                        qv[4 * u + 2] = lo32(Qn.y);
+                        qv[4 * u + 3] = hi32(Qn.y);
+                    }
+                    if constexpr (!UNIFORM) {
+                        if (full) tm_st16(tcol + S::COL_Q + 16 * k, qv);
+                        else tm_st4(tcol + S::COL_Q + 16 * k, qv[0], qv[1], qv[2], qv[3]);
+                    }
+                }
+#else
 #pragma unroll
                 for (int k0 = 0; k0 < NCHK; k0 += 2) {
                     double h[8], w[8], gr[8];
@@ -497,6 +584,7 @@ __global__ void __launch_bounds__(NW * (L2 / 16), 1)
                         }
                     }
                 }
+#endif
                 gsync();  // terms visible
                 // bin sums in ascending j.  Sixteen bins per thread, about one sample per bin:
                 // all bin ranges first, then every bin's first and second term as two batches
