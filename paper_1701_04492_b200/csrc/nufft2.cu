@@ -464,6 +464,10 @@ __global__ void __launch_bounds__(512, 1)
                 if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 gsync();
             });
+            // the last inter-pass twiddle factor in registers first: the products do not depend on
+            // the barrier below, so they fill the wait for the group's slowest warp
+#pragma unroll
+            for (int b = 1; b < 16; ++b) v[b] = cmul(v[b], step[b]);
 #if NB_P1_STAGE_WARP
             __syncwarp();  // the warp's exchange reads are done: its regions become its part of the box
 #else
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(512, 1)
 #endif
             NB_T1(t1_fft)
 #pragma unroll
-            for (int b = 0; b < 16; ++b) stg[kStgStride * b] = b == 0 ? v[0] : cmul(v[b], step[b]);
+            for (int b = 0; b < 16; ++b) stg[kStgStride * b] = v[b];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             gsync();  // box complete
 #ifdef NB_P1_SKIP_TMA  // timing ablation only (no output)
