@@ -316,6 +316,32 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- B200 arm
+def bind_to_gpu_numa_node(gpu: int):
+    """Run this process (and the pinned host buffers it allocates from here on) on the NUMA node
+    the GPU hangs off, as a deployment would with numactl: the end-to-end figures stream
+    2 x 2 GiB per step over PCIe, and a far-socket host buffer measured 1.7 instead of 2.6e9
+    points/s on some boxes of the pool.  Best effort; returns a description for the JSON line."""
+    try:
+        bus = subprocess.run(["nvidia-smi", "-i", str(gpu), "--query-gpu=pci.bus_id", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=10).stdout.strip().lower()
+        if bus.startswith("0000") and len(bus.split(":")[0]) == 8:
+            bus = bus[4:]  # sysfs uses a 4-digit domain
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read().strip())
+        if node < 0:
+            return "single NUMA node (no binding)"
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return f"GPU on NUMA node {node}, none of its CPUs allowed (no binding)"
+        os.sched_setaffinity(0, cpus)
+        return f"bound to NUMA node {node} of the GPU ({len(cpus)} CPUs)"
+    except Exception as e:  # noqa: BLE001 - measurement hygiene only
+        return f"not bound ({type(e).__name__})"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -323,6 +349,7 @@ def run_ours(args):
     import paper_1701_04492_b200 as nb
 
     world, rank, local = dist_env()
+    affinity = bind_to_gpu_numa_node(local)
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
@@ -457,7 +484,8 @@ def run_ours(args):
            "h2d_bytes_per_step": 16 * n * eb, "d2h_bytes_per_step": 16 * n * eb,
            "ms_per_step": e_s * 1e3,
            "api": "nufft_plan2_exec_host (pinned host buffers; batch > 1 pipelines H2D/transform/D2H); "
-                  "median of the timed calls"}
+                  "median of the timed calls",
+           "host_affinity": affinity}
     e1 = e2e_measure(1)
     e2e["batch1_pinned"] = {"value": n * world / e1, "ms_per_step": e1 * 1e3}
     # ---- e2e (2): exactly what a C++ user of the reference gets — the drop-in

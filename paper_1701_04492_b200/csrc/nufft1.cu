@@ -119,12 +119,21 @@ __global__ void __launch_bounds__(kDotThreads)
     }
     if (threadIdx.x < nr) part[(long long)blockIdx.x * kDotTerms + threadIdx.x] = red[threadIdx.x][0];
 }
-__global__ void k3_beta_dot_final(const double2* __restrict__ part, int r0, int nr, double2* __restrict__ D) {
-    const int q = threadIdx.x;
+// stage 2: one warp per term; lane l adds the blocks b = l, l + 32, ... in ascending order and
+// the lanes are combined by a fixed xor tree — a fixed order, so D is bit-reproducible.  (One
+// thread per term walking the 592 partials took ~0.12 ms per launch: dependent-latency bound.)
+__global__ void __launch_bounds__(32 * kDotTerms)
+    k3_beta_dot_final(const double2* __restrict__ part, int r0, int nr, double2* __restrict__ D) {
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (q >= nr) return;
     double2 s = make_double2(0.0, 0.0);
-    for (int b = 0; b < kDotBlocks; ++b) s = cadd(s, part[(long long)b * kDotTerms + q]);
-    D[r0 + q] = s;
+    for (int b = lane; b < kDotBlocks; b += 32) s = cadd(s, part[(long long)b * kDotTerms + q]);
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, m);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, m);
+    }
+    if (lane == 0) D[r0 + q] = s;
 }
 
 // f[j] = sum_r u^A_r(delta_j) Z_r,j with Z_r,j = y_r[t_j] (beta_j = 0) or D_r
@@ -253,7 +262,7 @@ void exec_type3(const Plan3State& p, const double2* c, double2* f, size_t batch,
                 k3_beta_dot_part<<<kDotBlocks, kDotThreads, 0, s>>>(cb, p.omega.as<double>(), (long long)N, (int)q0,
                                                                      nr, uni, part.as<double2>());
                 NB_LAUNCH();
-                k3_beta_dot_final<<<1, 32, 0, s>>>(part.as<double2>(), (int)q0, nr, D.as<double2>());
+                k3_beta_dot_final<<<1, 32 * kDotTerms, 0, s>>>(part.as<double2>(), (int)q0, nr, D.as<double2>());
                 NB_LAUNCH();
             }
         } else {
